@@ -1,0 +1,354 @@
+/*
+ * raas_ref.c — CPU ORACLE for page-based RaaS decode.  TEST INFRASTRUCTURE ONLY
+ * (see raas_ref.h).  Plain, slow, fp64, one unit at a time; no blocking, no fusion,
+ * no streaming softmax.  Each block cites the passage it follows.
+ *
+ * Algorithm (readings D1-D20 in DESIGN.md §3):
+ *   prefill(P):  pages 0..Pp-1 hold positions 1..P in order, 16 per page; they are
+ *                pinned ("Pages corresponding to prefill tokens are exempt from
+ *                eviction", App. B :396); t = P (time = number of tokens,
+ *                :394).
+ *   decode step: t += 1                                   (:394; Fig 5 row 5 -> ts 5, :100)
+ *                slot = current page if not full, else a fresh page if the budget
+ *                allows, else evict argmin_{unpinned} (ts, start_pos)
+ *                                                         (:29, :98 "evict tokens with the
+ *                                                          oldest timestamp"; :396; D9-D12)
+ *                write k,v; a written unpinned page gets ts = t (D8)
+ *                attend over all resident tokens          (standard attention, :46-48, :70)
+ *                stamp every unpinned page holding a token with normalised score > alpha
+ *                                                         (:29, :98, :364; D2-D5)
+ */
+#include "raas_ref.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+enum { REF_OK = 0, REF_E_INVALID = 1, REF_E_STATE = 3, REF_E_BUDGET = 4 };
+
+typedef struct {
+  int32_t *start, *count, *ts;
+  uint8_t *pinned;
+  double *K, *V;          /* [C][page][d] */
+  int32_t used, cur, t;
+  int32_t evicted, slot;  /* trace of the last step */
+  double *pstar;          /* [C] */
+} ref_unit;
+
+struct raas_ref {
+  raas_ref_config cfg;
+  int32_t C, units, g;
+  double scale;
+  int prefilled;
+  ref_unit* u;
+};
+
+static int g_threads = 1;
+
+int raas_ref_set_threads(int n) {
+#ifdef _OPENMP
+  if (n <= 0) n = omp_get_num_procs();
+  g_threads = n;
+#else
+  (void)n;
+  g_threads = 1;
+#endif
+  return g_threads;
+}
+
+/* bf16 bit pattern -> exact double (bf16 is the top half of an IEEE binary32). */
+static double widen_bf16(uint16_t b) {
+  uint32_t x = ((uint32_t)b) << 16;
+  float f;
+  memcpy(&f, &x, sizeof f);
+  return (double)f;
+}
+
+int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
+  if (!cfg || !out) return REF_E_INVALID;
+  if (cfg->L <= 0 || cfg->page <= 0 || cfg->L % cfg->page != 0) return REF_E_INVALID;
+  if (cfg->n_q_heads <= 0 || cfg->n_kv_heads <= 0 || cfg->n_q_heads % cfg->n_kv_heads != 0)
+    return REF_E_INVALID;
+  if (cfg->head_dim <= 0 || cfg->batch <= 0) return REF_E_INVALID;
+  if (!(cfg->alpha >= 0.0)) return REF_E_INVALID;
+  raas_ref* h = (raas_ref*)calloc(1, sizeof *h);
+  if (!h) return REF_E_INVALID;
+  h->cfg = *cfg;
+  h->C = cfg->L / cfg->page;
+  h->units = cfg->batch * cfg->n_kv_heads;
+  h->g = cfg->n_q_heads / cfg->n_kv_heads;
+  h->scale = cfg->softmax_scale != 0.0 ? cfg->softmax_scale : 1.0 / sqrt((double)cfg->head_dim);
+  h->u = (ref_unit*)calloc((size_t)h->units, sizeof(ref_unit));
+  size_t kv = (size_t)h->C * cfg->page * cfg->head_dim;
+  for (int32_t i = 0; i < h->units; ++i) {
+    ref_unit* u = &h->u[i];
+    u->start = (int32_t*)calloc((size_t)h->C, sizeof(int32_t));
+    u->count = (int32_t*)calloc((size_t)h->C, sizeof(int32_t));
+    u->ts = (int32_t*)calloc((size_t)h->C, sizeof(int32_t));
+    u->pinned = (uint8_t*)calloc((size_t)h->C, 1);
+    u->pstar = (double*)calloc((size_t)h->C, sizeof(double));
+    u->K = (double*)calloc(kv, sizeof(double));
+    u->V = (double*)calloc(kv, sizeof(double));
+    u->cur = -1;
+    u->evicted = -1;
+    u->slot = -1;
+  }
+  *out = h;
+  return REF_OK;
+}
+
+void raas_ref_destroy(raas_ref* h) {
+  if (!h) return;
+  for (int32_t i = 0; i < h->units; ++i) {
+    ref_unit* u = &h->u[i];
+    free(u->start); free(u->count); free(u->ts); free(u->pinned);
+    free(u->pstar); free(u->K); free(u->V);
+  }
+  free(h->u);
+  free(h);
+}
+
+/* Prefill (§2.1 :46 "computing and caching the key and value vectors for each
+ * token"; App. B :396 prefill pages exempt).  Positions 1..P, 16 per page (:147). */
+int raas_ref_prefill(raas_ref* h, const uint16_t* k, const uint16_t* v, int32_t P) {
+  if (!h || P < 0 || (P > 0 && (!k || !v))) return REF_E_INVALID;
+  if (h->prefilled) return REF_E_STATE;
+  const int32_t page = h->cfg.page, d = h->cfg.head_dim, C = h->C;
+  const int32_t Pp = (P + page - 1) / page;
+  if (Pp >= C) return REF_E_BUDGET;               /* D14: at least one decode page */
+  for (int32_t ui = 0; ui < h->units; ++ui) {
+    ref_unit* u = &h->u[ui];
+    for (int32_t j = 0; j < P; ++j) {             /* token j has position j+1 */
+      int32_t p = j / page, off = j % page;
+      for (int32_t c = 0; c < d; ++c) {
+        u->K[((size_t)p * page + off) * d + c] = widen_bf16(k[((size_t)ui * P + j) * d + c]);
+        u->V[((size_t)p * page + off) * d + c] = widen_bf16(v[((size_t)ui * P + j) * d + c]);
+      }
+    }
+    for (int32_t p = 0; p < Pp; ++p) {
+      u->start[p] = p * page + 1;
+      u->count[p] = (P - p * page) < page ? (P - p * page) : page;
+      u->ts[p] = 0;                               /* D17: pinned pages' ts untracked */
+      u->pinned[p] = 1;
+    }
+    u->used = Pp;
+    u->cur = Pp - 1;                              /* -1 when P == 0 */
+    u->t = P;
+    u->evicted = -1;
+    u->slot = -1;
+  }
+  h->prefilled = 1;
+  return REF_OK;
+}
+
+/* Slot selection and in-place write for one unit (D9-D13).
+ * Returns the slot; records the eviction. */
+static int32_t select_and_write(raas_ref* h, ref_unit* u, const uint16_t* kn, const uint16_t* vn) {
+  const int32_t page = h->cfg.page, d = h->cfg.head_dim, C = h->C;
+  u->t += 1;                                      /* time counts this token (:394) */
+  u->evicted = -1;
+  int32_t slot;
+  if (u->cur >= 0 && u->count[u->cur] < page) {
+    slot = u->cur;                                /* keep filling (also D13) */
+  } else {
+    if (u->used < C) {
+      slot = u->used;                             /* budget not reached (:100 first steps) */
+      u->used += 1;
+    } else {
+      /* "When the cache is full, we evict tokens with the oldest timestamp" (:29, :98);
+       * prefill exempt (:396); ties -> smallest start_pos (D12). */
+      slot = -1;
+      for (int32_t p = 0; p < C; ++p) {
+        if (u->pinned[p]) continue;
+        if (slot < 0 || u->ts[p] < u->ts[slot] ||
+            (u->ts[p] == u->ts[slot] && u->start[p] < u->start[slot]))
+          slot = p;
+      }
+      u->evicted = u->start[slot];
+    }
+    u->count[slot] = 0;                           /* the evicted tokens vanish here (D9) */
+    u->pinned[slot] = 0;
+    u->start[slot] = u->t;
+  }
+  int32_t off = u->count[slot];
+  if (kn && vn) {
+    for (int32_t c = 0; c < d; ++c) {
+      u->K[((size_t)slot * page + off) * d + c] = widen_bf16(kn[c]);
+      u->V[((size_t)slot * page + off) * d + c] = widen_bf16(vn[c]);
+    }
+  }
+  u->count[slot] += 1;
+  if (!u->pinned[slot]) u->ts[slot] = u->t;       /* a written page carries its write time (D8) */
+  u->cur = slot;
+  u->slot = slot;
+  return slot;
+}
+
+static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16_t* k_new,
+                        const uint16_t* v_new, double* out) {
+  const int32_t page = h->cfg.page, d = h->cfg.head_dim, C = h->C, g = h->g;
+  const int32_t Hq = h->cfg.n_q_heads, Hkv = h->cfg.n_kv_heads;
+  const int32_t b = ui / Hkv, kvh = ui % Hkv;
+  ref_unit* u = &h->u[ui];
+  select_and_write(h, u, k_new + (size_t)ui * d, v_new + (size_t)ui * d);
+
+  double* s = (double*)malloc((size_t)C * page * sizeof(double));
+  double* best = (double*)malloc((size_t)C * sizeof(double));
+  double* qh = (double*)malloc((size_t)d * sizeof(double));
+  for (int32_t p = 0; p < C; ++p) best[p] = -INFINITY;
+
+  for (int32_t hh = 0; hh < g; ++hh) {            /* q-head h uses kv-head floor(h/g) (D15) */
+    const int32_t qi = b * Hq + kvh * g + hh;
+    for (int32_t c = 0; c < d; ++c) qh[c] = widen_bf16(q[(size_t)qi * d + c]);
+    /* scores s_j = scale * <q, k_j> over every resident token (D2, D20) */
+    double mx = -INFINITY;
+    for (int32_t p = 0; p < C; ++p)
+      for (int32_t i = 0; i < u->count[p]; ++i) {
+        const double* kj = &u->K[((size_t)p * page + i) * d];
+        double acc = 0.0;
+        for (int32_t c = 0; c < d; ++c) acc += qh[c] * kj[c];
+        s[p * page + i] = h->scale * acc;
+        if (s[p * page + i] > mx) mx = s[p * page + i];
+      }
+    /* LSE = log sum_j exp(s_j)  (softmax normaliser, :70) */
+    double sum = 0.0;
+    for (int32_t p = 0; p < C; ++p)
+      for (int32_t i = 0; i < u->count[p]; ++i) sum += exp(s[p * page + i] - mx);
+    const double lse = mx + log(sum);
+    if (out) {
+      double* o = out + (size_t)qi * d;
+      for (int32_t c = 0; c < d; ++c) o[c] = 0.0;
+      for (int32_t p = 0; p < C; ++p)
+        for (int32_t i = 0; i < u->count[p]; ++i) {
+          const double w = exp(s[p * page + i] - lse);
+          const double* vj = &u->V[((size_t)p * page + i) * d];
+          for (int32_t c = 0; c < d; ++c) o[c] += w * vj[c];
+        }
+    }
+    /* decisive log-probability per page: max over heads of the group and tokens (D4, D5) */
+    for (int32_t p = 0; p < C; ++p) {
+      if (u->pinned[p]) continue;
+      for (int32_t i = 0; i < u->count[p]; ++i) {
+        const double lp = s[p * page + i] - lse;
+        if (lp > best[p]) best[p] = lp;
+      }
+    }
+  }
+  /* stamp: "we assign it the latest timestamp" when the score is above alpha (:29, :98,
+   * :364), strictly (D3), in the log domain s - LSE > ln(alpha) (D2). */
+  const double ln_alpha = log(h->cfg.alpha);     /* alpha = 0 -> -inf: every page stamped */
+  for (int32_t p = 0; p < C; ++p) {
+    u->pstar[p] = -1.0;
+    if (u->pinned[p] || u->count[p] == 0) continue;
+    u->pstar[p] = exp(best[p]);
+    if (best[p] > ln_alpha) u->ts[p] = u->t;
+  }
+  free(s); free(best); free(qh);
+}
+
+int raas_ref_decode_step(raas_ref* h, const uint16_t* q, const uint16_t* k_new,
+                         const uint16_t* v_new, double* out) {
+  if (!h || !q || !k_new || !v_new) return REF_E_INVALID;
+  if (!h->prefilled) return REF_E_STATE;
+  int32_t ui;
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+  for (ui = 0; ui < h->units; ++ui) decode_unit(h, ui, q, k_new, v_new, out);
+  return REF_OK;
+}
+
+int raas_ref_step_stamps(raas_ref* h, const uint8_t* stamps) {
+  if (!h || !stamps) return REF_E_INVALID;
+  if (!h->prefilled) return REF_E_STATE;
+  for (int32_t ui = 0; ui < h->units; ++ui) {
+    ref_unit* u = &h->u[ui];
+    select_and_write(h, u, NULL, NULL);
+    for (int32_t p = 0; p < h->C; ++p) {
+      u->pstar[p] = -1.0;
+      if (u->pinned[p] || u->count[p] == 0) continue;
+      if (stamps[(size_t)ui * h->C + p]) u->ts[p] = u->t;
+    }
+  }
+  return REF_OK;
+}
+
+int raas_ref_get_state(const raas_ref* h, int32_t* t, int32_t* ts, int32_t* start_pos,
+                       int32_t* count, uint8_t* pinned) {
+  if (!h) return REF_E_INVALID;
+  const int32_t C = h->C;
+  for (int32_t ui = 0; ui < h->units; ++ui) {
+    const ref_unit* u = &h->u[ui];
+    if (t) t[ui] = u->t;
+    if (ts) memcpy(ts + (size_t)ui * C, u->ts, (size_t)C * sizeof(int32_t));
+    if (start_pos) memcpy(start_pos + (size_t)ui * C, u->start, (size_t)C * sizeof(int32_t));
+    if (count) memcpy(count + (size_t)ui * C, u->count, (size_t)C * sizeof(int32_t));
+    if (pinned) memcpy(pinned + (size_t)ui * C, u->pinned, (size_t)C);
+  }
+  return REF_OK;
+}
+
+int raas_ref_set_state(raas_ref* h, const int32_t* t, const int32_t* ts,
+                       const int32_t* start_pos, const int32_t* count, const uint8_t* pinned,
+                       const uint16_t* k_store, const uint16_t* v_store) {
+  if (!h || !t || !ts || !start_pos || !count || !pinned) return REF_E_INVALID;
+  const int32_t C = h->C, page = h->cfg.page, d = h->cfg.head_dim;
+  const size_t kv = (size_t)C * page * d;
+  for (int32_t ui = 0; ui < h->units; ++ui) {
+    ref_unit* u = &h->u[ui];
+    u->t = t[ui];
+    memcpy(u->ts, ts + (size_t)ui * C, (size_t)C * sizeof(int32_t));
+    memcpy(u->start, start_pos + (size_t)ui * C, (size_t)C * sizeof(int32_t));
+    memcpy(u->count, count + (size_t)ui * C, (size_t)C * sizeof(int32_t));
+    memcpy(u->pinned, pinned + (size_t)ui * C, (size_t)C);
+    u->used = 0;
+    u->cur = -1;
+    for (int32_t p = 0; p < C; ++p) {
+      if (u->count[p] > 0) {
+        u->used += 1;
+        if (u->cur < 0 || u->start[p] > u->start[u->cur]) u->cur = p;
+      }
+    }
+    if (k_store)
+      for (size_t i = 0; i < kv; ++i) u->K[i] = widen_bf16(k_store[(size_t)ui * kv + i]);
+    if (v_store)
+      for (size_t i = 0; i < kv; ++i) u->V[i] = widen_bf16(v_store[(size_t)ui * kv + i]);
+    u->evicted = -1;
+    u->slot = -1;
+  }
+  h->prefilled = 1;
+  return REF_OK;
+}
+
+int raas_ref_get_trace(const raas_ref* h, int32_t* evicted, int32_t* slot, double* pstar) {
+  if (!h) return REF_E_INVALID;
+  for (int32_t ui = 0; ui < h->units; ++ui) {
+    const ref_unit* u = &h->u[ui];
+    if (evicted) evicted[ui] = u->evicted;
+    if (slot) slot[ui] = u->slot;
+    if (pstar) memcpy(pstar + (size_t)ui * h->C, u->pstar, (size_t)h->C * sizeof(double));
+  }
+  return REF_OK;
+}
+
+int raas_ref_resident_positions(const raas_ref* h, int32_t unit, int32_t* pos, int32_t cap) {
+  if (!h || unit < 0 || unit >= h->units) return -1;
+  const ref_unit* u = &h->u[unit];
+  int32_t n = 0;
+  /* gather, then insertion-sort ascending (tiny sizes only) */
+  for (int32_t p = 0; p < h->C; ++p)
+    for (int32_t i = 0; i < u->count[p]; ++i) {
+      if (n < cap && pos) pos[n] = u->start[p] + i;
+      n++;
+    }
+  if (pos) {
+    int32_t m = n < cap ? n : cap;
+    for (int32_t a = 1; a < m; ++a) {
+      int32_t x = pos[a], b = a - 1;
+      while (b >= 0 && pos[b] > x) { pos[b + 1] = pos[b]; --b; }
+      pos[b + 1] = x;
+    }
+  }
+  return n;
+}

@@ -1,0 +1,78 @@
+/*
+ * raas_ref.h — CPU ORACLE for the RaaS decode hot path.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library.  The product (libraas, include/raas.h) never links,
+ * includes or calls it, and it shares no code with the CUDA path.
+ *
+ * What it computes: page-based RaaS (§3.3 :143-151, App. B :358-398) one
+ * decode step at a time, in fp64, following SURVEY.md §8(c1) step by step, with the
+ * readings D1-D20 listed in DESIGN.md §3.  Every tensor is a HOST buffer; bf16 values
+ * are passed as their raw uint16 bit patterns and widened exactly to double.
+ *
+ * Layouts (row-major):
+ *   q, out      [batch][n_q_heads][head_dim]
+ *   k, v        [batch][n_kv_heads][P][head_dim]       (prefill)
+ *   k_new,v_new [batch][n_kv_heads][head_dim]
+ *   state arrays [batch*n_kv_heads][C]  with C = L / page ("unit" = (request, kv-head))
+ *
+ * Return codes: 0 OK, 1 invalid argument, 3 state error (decode before prefill,
+ * prefill twice), 4 budget (ceil(P/page) >= C, reading D14).
+ */
+#ifndef RAAS_REF_H
+#define RAAS_REF_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t L;             /* token budget per unit, includes prefill (PAPER.md :173) */
+  double  alpha;         /* stamp iff normalised score > alpha (:29, :169 default 1e-4) */
+  int32_t page;          /* tokens per page (:147, 16); 1 = token-level RaaS of §3.2 */
+  int32_t n_q_heads;
+  int32_t n_kv_heads;
+  int32_t head_dim;
+  int32_t batch;
+  double  softmax_scale; /* 0 => 1/sqrt(head_dim) */
+} raas_ref_config;
+
+typedef struct raas_ref raas_ref;
+
+int  raas_ref_create(const raas_ref_config* cfg, raas_ref** out);
+void raas_ref_destroy(raas_ref* h);
+int  raas_ref_prefill(raas_ref* h, const uint16_t* k, const uint16_t* v, int32_t P);
+/* one decode step for every unit; out may be NULL */
+int  raas_ref_decode_step(raas_ref* h, const uint16_t* q, const uint16_t* k_new,
+                          const uint16_t* v_new, double* out);
+/* bookkeeping-only step (pin P5): slot selection + write as in decode_step, but the
+ * stamp decisions are GIVEN: stamps[unit*C + p] != 0 stamps page p (ignored for pinned
+ * or empty pages).  No K/V data is written or attended. */
+int  raas_ref_step_stamps(raas_ref* h, const uint8_t* stamps);
+
+/* state readout; any pointer may be NULL.  t[unit] = tokens so far (PAPER.md :394). */
+int  raas_ref_get_state(const raas_ref* h, int32_t* t, int32_t* ts, int32_t* start_pos,
+                        int32_t* count, uint8_t* pinned);
+/* lockstep resync (SURVEY §8c parity protocol): overwrite metadata and, when non-NULL,
+ * the KV store (bf16 bits, [units][C][page][head_dim]).  cur/used are re-derived. */
+int  raas_ref_set_state(raas_ref* h, const int32_t* t, const int32_t* ts,
+                        const int32_t* start_pos, const int32_t* count,
+                        const uint8_t* pinned, const uint16_t* k_store,
+                        const uint16_t* v_store);
+/* trace of the LAST step:
+ *   evicted[unit]  = start_pos of the page evicted before attention, or -1
+ *   slot[unit]     = page index the new token was written to
+ *   pstar[unit*C+p]= max_{h in group, j in p} p_{h,j} for unpinned resident pages,
+ *                    -1 otherwise (used for the |p*-alpha| exactness band) */
+int  raas_ref_get_trace(const raas_ref* h, int32_t* evicted, int32_t* slot, double* pstar);
+/* resident token positions of one unit after the last step, ascending; returns count */
+int  raas_ref_resident_positions(const raas_ref* h, int32_t unit, int32_t* pos, int32_t cap);
+/* threads used by the OpenMP loop over units (1 = serial); returns the effective count */
+int  raas_ref_set_threads(int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

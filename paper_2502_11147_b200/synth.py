@@ -1,0 +1,148 @@
+"""Seeded synthetic inputs for the RaaS decode path (shared by tests, oracle runs, bench).
+
+This module holds NO arithmetic of the method (no attention, no timestamps, no
+eviction): it only draws q / k / v streams and rounds them to bf16.  Both the CUDA path
+and the CPU oracle consume exactly the bf16 bit patterns produced here.
+
+Recipes:
+
+* ``gaussian_stream`` — i.i.d. N(0, sigma^2) q/k/v.  Page-level stamping is ~100% on this
+  data, so it exercises the attention numerics, not the eviction policy.
+* ``waterfall_stream`` — the "waterfall" pattern of PAPER.md §3.1 (:27, :88-94, Fig 3
+  :108): a sink page (the "lazy" StreamingLLM pattern, >70% of maps), the two most
+  recent pages, milestone decode pages that emerge and fade (20-25% of maps; decay
+  half-life 256 steps) and rare phoenix reactivations of prefill pages (1-2%, gaps >128
+  steps).  Keys of one logical page share a signature vector, so page-level stamping
+  is selective (30-60% of pages at the calibrated lambda), which is what makes eviction
+  non-trivial.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+PAGE = 16
+
+
+def bf16_bits(x) -> np.ndarray:
+    """Round float32 -> bf16 (round-to-nearest-even) and return the uint16 bit patterns."""
+    f = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    u = f.view(np.uint32).astype(np.uint64)
+    rounded = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    nan = np.isnan(f)
+    out = rounded.astype(np.uint16)
+    if nan.any():
+        out[nan] = 0x7FC0
+    return out
+
+
+def bf16_to_f32(bits) -> np.ndarray:
+    b = np.ascontiguousarray(np.asarray(bits, dtype=np.uint16))
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+class Stream:
+    """A full decode workload: prefill K/V plus T steps of (q, k_new, v_new), as bf16 bits.
+
+    Shapes: k_pre, v_pre [B, Hkv, P, d]; q [T, B, Hq, d]; k, v [T, B, Hkv, d].
+    """
+
+    def __init__(self, k_pre, v_pre, q, k, v):
+        self.k_pre, self.v_pre, self.q, self.k, self.v = k_pre, v_pre, q, k, v
+
+    @property
+    def T(self):
+        return self.q.shape[0]
+
+    @property
+    def P(self):
+        return self.k_pre.shape[2]
+
+
+def gaussian_stream(seed, B, Hq, Hkv, d, P, T, sigma_q=1.0, sigma_k=1.0, sigma_v=1.0) -> Stream:
+    rng = np.random.Generator(np.random.Philox(seed))
+    k_pre = bf16_bits(rng.standard_normal((B, Hkv, P, d), np.float32) * sigma_k)
+    v_pre = bf16_bits(rng.standard_normal((B, Hkv, P, d), np.float32) * sigma_v)
+    q = bf16_bits(rng.standard_normal((T, B, Hq, d), np.float32) * sigma_q)
+    k = bf16_bits(rng.standard_normal((T, B, Hkv, d), np.float32) * sigma_k)
+    v = bf16_bits(rng.standard_normal((T, B, Hkv, d), np.float32) * sigma_v)
+    return Stream(k_pre, v_pre, q, k, v)
+
+
+def waterfall_stream(seed, B, Hq, Hkv, d, P, T, lam=6.0, eta=1.0, key_noise=0.5,
+                     p_milestone=0.1, milestone_half_life=256.0, p_phoenix=1.0 / 512,
+                     phoenix_len=32, recent_weight=0.8, phoenix_weight=0.8) -> Stream:
+    """Waterfall-shaped stream (§3.1, Fig 3).  Positions are 1-based; the
+    logical page of position j is (j-1)//16 (a property of the workload, not of the
+    cache: the generator does not know what the cache retained)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    g = Hq // Hkv
+    U = B * Hkv
+    n_tok = P + T
+    n_pages = (n_tok + PAGE - 1) // PAGE
+    phi = rng.standard_normal((U, n_pages, d)).astype(np.float64)
+    phi /= np.linalg.norm(phi, axis=-1, keepdims=True)
+    page_of = np.arange(n_tok) // PAGE                       # position j+1 -> page
+    keys = phi[:, page_of, :] + key_noise * rng.standard_normal((U, n_tok, d)) / np.sqrt(d)
+    vals = rng.standard_normal((U, n_tok, d))
+    pp = (P + PAGE - 1) // PAGE                              # pages touched by the prompt
+    # milestones: a page that starts inside the decode becomes one with prob p_milestone
+    first_pos = np.arange(n_pages) * PAGE + 1
+    is_dec_page = first_pos > P
+    ms = (rng.random((U, n_pages)) < p_milestone) & is_dec_page[None, :]
+    ms_strength = rng.uniform(0.2, 1.0, (U, n_pages)) * ms
+    phoenix_until = np.full(U, -1, np.int64)
+    phoenix_page = np.zeros(U, np.int64)
+    q = np.empty((T, B, Hq, d), np.float32)
+    for i in range(T):
+        t = P + i + 1                                        # position of the new token
+        cur = (t - 1) // PAGE
+        w = np.zeros((U, n_pages))
+        w[:, 0] = 1.0                                        # sink ("lazy" maps)
+        w[:, cur] = np.maximum(w[:, cur], recent_weight)
+        if cur >= 1:
+            w[:, cur - 1] = np.maximum(w[:, cur - 1], recent_weight)
+        age = t - first_pos[None, : cur + 1]
+        decay = np.where(age >= 0, 2.0 ** (-np.maximum(age, 0) / milestone_half_life), 0.0)
+        w[:, : cur + 1] = np.maximum(w[:, : cur + 1], ms_strength[:, : cur + 1] * decay)
+        if pp > 0:
+            start = (rng.random(U) < p_phoenix) & (phoenix_until < t)
+            phoenix_page[start] = rng.integers(0, pp, int(start.sum()))
+            phoenix_until[start] = t + phoenix_len
+            act = phoenix_until >= t
+            w[act, phoenix_page[act]] = np.maximum(w[act, phoenix_page[act]], phoenix_weight)
+        base = lam * np.sqrt(d) * np.einsum("up,upd->ud", w, phi)
+        noise = eta * rng.standard_normal((U, g, d))
+        q[i] = (base[:, None, :] + noise).reshape(B, Hkv * g, d)
+    keys = keys.reshape(B, Hkv, n_tok, d).astype(np.float32)
+    vals = vals.reshape(B, Hkv, n_tok, d).astype(np.float32)
+    k_pre = bf16_bits(keys[:, :, :P])
+    v_pre = bf16_bits(vals[:, :, :P])
+    k = bf16_bits(np.moveaxis(keys[:, :, P:], 2, 0))
+    v = bf16_bits(np.moveaxis(vals[:, :, P:], 2, 0))
+    return Stream(k_pre, v_pre, bf16_bits(q), k, v)
+
+
+def random_steady_state(seed, units, C, Pp, t_now, page=PAGE):
+    """A full-cache state for bounded-sample timing (bench CPU baseline): pinned prefill
+    pages 0..Pp-1, C-Pp full decode pages of 16 consecutive positions each, the newest
+    one ending at t_now, timestamps in [end of page, t_now].  Draws numbers only; the
+    method's rules are not applied here.  Requires t_now >= Pp*page + 4*page*(C-Pp)."""
+    nd = C - Pp
+    assert t_now >= Pp * page + 4 * page * nd, "t_now too small for the spread"
+    rng = np.random.Generator(np.random.Philox(seed))
+    ts = np.zeros((units, C), np.int32)
+    start = np.zeros((units, C), np.int32)
+    count = np.full((units, C), page, np.int32)
+    pinned = np.zeros((units, C), np.uint8)
+    pinned[:, :Pp] = 1
+    start[:, :Pp] = np.arange(Pp) * page + 1
+    for u in range(units):
+        offs = np.concatenate([[0], np.sort(rng.choice(np.arange(1, 4 * nd), nd - 1, replace=False))])
+        starts = t_now - page + 1 - page * offs
+        ts_u = np.minimum(t_now, starts + page - 1 + rng.integers(0, 64, nd))
+        ts_u[0] = t_now
+        perm = rng.permutation(nd)
+        start[u, Pp:] = starts[perm]
+        ts[u, Pp:] = ts_u[perm]
+    t = np.full(units, t_now, np.int32)
+    return dict(t=t, ts=ts, start=start, count=count, pinned=pinned)

@@ -1,0 +1,442 @@
+"""Pins for the CPU oracle: each check is fixed by the paper or
+by mathematics, never by the oracle itself.  CPU only."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from paper_2502_11147_b200.synth import bf16_to_f32, gaussian_stream, waterfall_stream
+from traces import hand_trace_stream, page_twin_stream
+
+PAGE = 16
+
+
+def run_oracle(oracle_mod, stream, L, alpha, page, Hq, Hkv, on_step=None):
+    B, _, P, d = stream.k_pre.shape
+    o = oracle_mod.Oracle(L=L, alpha=alpha, page=page, n_q_heads=Hq, n_kv_heads=Hkv,
+                          head_dim=d, batch=B)
+    o.prefill(stream.k_pre, stream.v_pre, P)
+    outs = []
+    for i in range(stream.T):
+        out = o.decode_step(stream.q[i], stream.k[i], stream.v[i])
+        outs.append(out)
+        if on_step is not None:
+            on_step(i, P + i + 1, o, out)
+    return o, outs
+
+
+def positions_kv(stream):
+    """K, V for every position 1..P+T as fp64 arrays [B, Hkv, N, d] (index pos-1)."""
+    K = np.concatenate([bf16_to_f32(stream.k_pre), np.moveaxis(bf16_to_f32(stream.k), 0, 2)], axis=2)
+    V = np.concatenate([bf16_to_f32(stream.v_pre), np.moveaxis(bf16_to_f32(stream.v), 0, 2)], axis=2)
+    return K.astype(np.float64), V.astype(np.float64)
+
+
+def textbook_attention(q, K, V, scale):
+    """softmax(scale * q K^T) V for one head, fp64 (Vaswani et al.; PAPER.md :70)."""
+    s = scale * (K @ q)
+    w = np.exp(s - s.max())
+    w /= w.sum()
+    return w @ V
+
+
+# ---------------------------------------------------------------- P3 hand trace
+
+
+def test_p3_hand_trace_token_level(oracle_mod):
+    g, st = hand_trace_stream()
+    s, exp = g["setup"], g["expected"]
+    evictions = []
+
+    def on_step(i, t, o, out):
+        ev = o.get_trace()["evicted"][0]
+        if ev >= 0:
+            evictions.append([t, int(ev)])
+
+    o, _ = run_oracle(oracle_mod, st, L=s["L"], alpha=s["alpha"], page=1, Hq=1, Hkv=1,
+                      on_step=on_step)
+    assert evictions == exp["evictions"]
+    assert o.resident_positions(0).tolist() == exp["final_resident"]
+    state = o.get_state()
+    ts_by_pos = {int(p): int(t) for p, t, pin in zip(state["start"][0], state["ts"][0], state["pinned"][0]) if not pin}
+    assert ts_by_pos == {int(k): v for k, v in exp["final_ts"].items()}
+
+
+def test_p3_fig5_narrative_facts(oracle_mod):
+    """The three facts PAPER.md :100 narrates, read off the same trace."""
+    g, st = hand_trace_stream()
+    s = g["setup"]
+    seen = {}
+
+    def on_step(i, t, o, out):
+        state = o.get_state()
+        seen[t] = {int(p): int(ts) for p, ts in zip(state["start"][0], state["ts"][0])}
+        seen[(t, "ev")] = int(o.get_trace()["evicted"][0])
+
+    run_oracle(oracle_mod, st, L=s["L"], alpha=s["alpha"], page=1, Hq=1, Hkv=1, on_step=on_step)
+    # token 4 is attended at t=5 but below alpha: not refreshed (Fig 5 row 4 analogue)
+    assert seen[5][4] == 4
+    # token 4 exceeds alpha at t=6: it gets the latest timestamp (Fig 5 row 5: "timestamp 5")
+    assert seen[6][4] == 6
+    # first full step evicts the oldest token (Fig 5 row 6) and the new token is resident
+    assert seen[(7, "ev")] == 3 and seen[7].get(7) == 7
+
+
+def test_p3_page_twin(oracle_mod):
+    for gh in (1, 4):
+        g, st = page_twin_stream(g_heads=gh, value_seed=3)
+        s, exp = g["setup"], g["expected"]
+        evictions = []
+
+        def on_step(i, t, o, out):
+            ev = o.get_trace()["evicted"][0]
+            if ev >= 0:
+                evictions.append([t, (int(ev) - 1) // PAGE + 1])
+
+        o, _ = run_oracle(oracle_mod, st, L=s["L"], alpha=s["alpha"], page=PAGE, Hq=gh, Hkv=1,
+                          on_step=on_step)
+        assert evictions == exp["page_evictions"]
+        state = o.get_state()
+        pages = sorted((int(sp) - 1) // PAGE + 1 for sp in state["start"][0])
+        assert pages == exp["final_pages"]
+        ts = {(int(sp) - 1) // PAGE + 1: int(t) for sp, t, pin in
+              zip(state["start"][0], state["ts"][0], state["pinned"][0]) if not pin}
+        assert ts == {int(k): v for k, v in exp["final_ts"].items()}
+
+
+# ---------------------------------------------------------------- P1 dense equivalence
+
+
+@pytest.mark.parametrize("kind,g,d,P", [("gauss", 4, 64, 37), ("water", 2, 64, 32), ("gauss", 1, 32, 5),
+                                        ("gauss", 7, 128, 16)])
+def test_p1_dense_equivalence(oracle_mod, kind, g, d, P):
+    """L >= P+T: nothing is evicted, so every step is textbook causal attention over all
+    tokens so far (§2.1 :46-48, :70)."""
+    B, Hkv, T = 2, 2, 40
+    Hq = g * Hkv
+    mk = gaussian_stream if kind == "gauss" else waterfall_stream
+    st = mk(11, B, Hq, Hkv, d, P, T)
+    L = ((P + T + PAGE - 1) // PAGE + 1) * PAGE
+    K, V = positions_kv(st)
+    scale = 1.0 / math.sqrt(d)
+    maxerr = 0.0
+
+    def on_step(i, t, o, out):
+        nonlocal maxerr
+        assert (o.get_trace()["evicted"] == -1).all()
+        q = bf16_to_f32(st.q[i]).astype(np.float64)
+        for b in range(B):
+            for h in range(Hq):
+                kv = h // g
+                ref = textbook_attention(q[b, h], K[b, kv, :t], V[b, kv, :t], scale)
+                maxerr = max(maxerr, np.abs(ref - out[b, h]).max())
+
+    run_oracle(oracle_mod, st, L=L, alpha=1e-4, page=PAGE, Hq=Hq, Hkv=Hkv, on_step=on_step)
+    assert maxerr < 1e-12
+
+
+# ---------------------------------------------------------------- P2 invariants + P8
+
+
+def test_p2_invariants_and_p8_resident_attention(oracle_mod):
+    """Every step: prefill resident, occupancy <= L, ts <= t, ts >= last write, pages hold
+    consecutive positions, evicted positions never return (no recall, D19), and `out`
+    equals textbook attention over exactly the resident positions (P8)."""
+    B, Hkv, g, d, P, T, L = 2, 2, 4, 64, 40, 300, 128
+    Hq = g * Hkv
+    st = waterfall_stream(5, B, Hq, Hkv, d, P, T, lam=6.0)
+    K, V = positions_kv(st)
+    scale = 1.0 / math.sqrt(d)
+    gone = [set() for _ in range(B * Hkv)]
+    prev = [None] * (B * Hkv)
+    n_ev = 0
+    stamped = []
+
+    def on_step(i, t, o, out):
+        nonlocal n_ev
+        state = o.get_state()
+        tr = o.get_trace()
+        q = bf16_to_f32(st.q[i]).astype(np.float64)
+        for u in range(B * Hkv):
+            res = o.resident_positions(u)
+            rs = set(res.tolist())
+            assert set(range(1, P + 1)) <= rs                     # prefill pinned (:396)
+            assert len(res) <= L                                   # O(L) memory (:191-193)
+            assert t in rs                                         # new token attended (D20)
+            assert len(rs) == len(res)
+            if prev[u] is not None:
+                gone[u] |= prev[u] - rs
+            assert not (gone[u] & rs)                              # no recall (D19)
+            prev[u] = rs
+            for p in range(o.C):
+                c, s0, ts, pin = (state["count"][u, p], state["start"][u, p], state["ts"][u, p],
+                                  state["pinned"][u, p])
+                if c == 0:
+                    continue
+                assert s0 + c - 1 <= t
+                if not pin:
+                    assert s0 + c - 1 <= ts <= t                   # ts >= last write (D8), <= now
+                    stamped.append(ts == t)
+            if tr["evicted"][u] >= 0:
+                n_ev += 1
+            b, kv = divmod(u, Hkv)
+            idx = res - 1
+            for j in range(g):
+                h = kv * g + j
+                ref = textbook_attention(q[b, h], K[b, kv, idx], V[b, kv, idx], scale)
+                assert np.abs(ref - out[b, h]).max() < 1e-12
+
+    run_oracle(oracle_mod, st, L=L, alpha=1e-4, page=PAGE, Hq=Hq, Hkv=Hkv, on_step=on_step)
+    assert n_ev > 0
+    rate = np.mean(stamped)
+    assert 0.05 < rate < 0.95, rate                                # waterfall data is selective
+
+
+# ---------------------------------------------------------------- P4 alpha in {0, >=1}
+
+
+def sliding_window(P, L, t, page=PAGE):
+    """StreamingLLM at page granularity (PAPER.md :70, :223): pinned prefill pages plus
+    the most recent C-Pp decode pages."""
+    C, Pp = L // page, -(-P // page)
+    B0 = Pp * page
+    if t <= B0:
+        return list(range(1, t + 1))
+    kc = (t - B0 - 1) // page
+    res = list(range(1, B0 + 1))
+    for k in range(max(0, kc - (C - Pp) + 1), kc + 1):
+        res += list(range(B0 + page * k + 1, min(B0 + page * k + page, t) + 1))
+    return res
+
+
+@pytest.mark.parametrize("P,L,T", [(32, 64, 256), (100, 128, 300), (20, 48, 100), (0, 32, 80)])
+@pytest.mark.parametrize("alpha", [0.0, 1.0, 3.0])
+def test_p4_alpha_extremes_are_sliding_window(oracle_mod, P, L, T, alpha):
+    st = gaussian_stream(7, 1, 2, 1, 16, P, T)
+
+    def on_step(i, t, o, out):
+        assert o.resident_positions(0).tolist() == sliding_window(P, L, t)
+        state = o.get_state()
+        unp = (state["pinned"][0] == 0) & (state["count"][0] > 0)
+        if alpha == 0.0:                       # ln 0 = -inf: every page stamped every step
+            assert (state["ts"][0][unp] == t).all()
+        else:                                  # s - LSE <= 0 <= ln(alpha): nothing stamped
+            last = state["start"][0] + state["count"][0] - 1
+            assert (state["ts"][0][unp] == last[unp]).all()
+
+    run_oracle(oracle_mod, st, L=L, alpha=alpha, page=PAGE, Hq=2, Hkv=1, on_step=on_step)
+
+
+# ---------------------------------------------------------------- P5 brute-force bookkeeping
+
+
+def brute_force_bookkeeping(P, L, page, stamp_steps):
+    """Reference recomputed from the full event history (PAPER.md :364, :394, :396):
+    a page's timestamp is the latest time it was written or stamped; the victim is the
+    unpinned page with the smallest (timestamp, first position).  Slots are filled
+    lowest-empty-first.  Returns per-step [(start, count, ts) per slot] and evictions."""
+    C, Pp = L // page, -(-P // page)
+    slots = [None] * C
+    for p in range(Pp):
+        pos = list(range(p * page + 1, min(p * page + page, P) + 1))
+        slots[p] = dict(pos=pos, events=[], pinned=True)
+    t, last_pos = P, P
+    hist = []
+    for stamps in stamp_steps:
+        t += 1
+        cur = None
+        for s, pg in enumerate(slots):
+            if pg is not None and last_pos in pg["pos"]:
+                cur = s
+        ev = -1
+        if cur is not None and len(slots[cur]["pos"]) < page:
+            slot = cur
+        else:
+            empty = [s for s, pg in enumerate(slots) if pg is None]
+            if empty:
+                slot = empty[0]
+            else:
+                cands = sorted((max(pg["events"]), pg["pos"][0], s)
+                               for s, pg in enumerate(slots) if not pg["pinned"])
+                slot = cands[0][2]
+                ev = slots[slot]["pos"][0]
+            slots[slot] = dict(pos=[], events=[], pinned=False)
+        slots[slot]["pos"].append(t)
+        slots[slot]["events"].append(t)
+        last_pos = t
+        for s in stamps:
+            if slots[s] is not None and not slots[s]["pinned"]:
+                slots[s]["events"].append(t)
+        snap = []
+        for pg in slots:
+            if pg is None:
+                snap.append((0, 0, 0))
+            else:
+                snap.append((pg["pos"][0], len(pg["pos"]), 0 if pg["pinned"] else max(pg["events"])))
+        hist.append((snap, ev))
+    return hist
+
+
+@pytest.mark.parametrize("page,P,L,T", [(1, 1, 4, 5), (2, 2, 6, 7), (2, 3, 8, 6), (1, 0, 3, 5)])
+def test_p5_bookkeeping_enumeration(oracle_mod, page, P, L, T):
+    C, Pp = L // page, -(-P // page)
+    dec = list(range(Pp, C))
+    nd = len(dec)
+    n = 1 << (nd * T)
+    o = oracle_mod.Oracle(L=L, alpha=1e-4, page=page, n_q_heads=1, n_kv_heads=1, head_dim=1, batch=n)
+    zeros = np.zeros((n, 1, P, 1), np.uint16)
+    o.prefill(zeros, zeros, P)
+    pats = np.arange(n, dtype=np.int64)
+    got = []
+    for i in range(T):
+        stamps = np.zeros((n, C), np.uint8)
+        for j, s in enumerate(dec):
+            stamps[:, s] = (pats >> (i * nd + j)) & 1
+        o.step_stamps(stamps)
+        got.append((o.get_state(), o.get_trace()["evicted"].copy()))
+    for u in range(n):
+        steps = [[dec[j] for j in range(nd) if (u >> (i * nd + j)) & 1] for i in range(T)]
+        ref = brute_force_bookkeeping(P, L, page, steps)
+        for i, (snap, ev) in enumerate(ref):
+            state, evs = got[i]
+            mine = list(zip(state["start"][u].tolist(), state["count"][u].tolist(),
+                            np.where(state["pinned"][u] == 1, 0, state["ts"][u]).tolist()))
+            assert mine == snap, (u, i)
+            assert evs[u] == ev, (u, i)
+
+
+# ---------------------------------------------------------------- P6 brute-force end-to-end
+
+
+def brute_force_end_to_end(stream, L, alpha, page, g):
+    """From-scratch simulator: token positions, direct exp/sum per step (no streaming
+    LSE), stamp iff exp(s - LSE) > alpha, evict min (ts, first position)."""
+    K, V = positions_kv(stream)
+    B, Hkv, P, d = stream.k_pre.shape
+    C, Pp = L // page, -(-P // page)
+    scale = 1.0 / math.sqrt(d)
+    res = []
+    for b in range(B):
+        for kv in range(Hkv):
+            pages = []  # dicts: positions, ts, pinned, slot
+            for p in range(Pp):
+                pages.append(dict(pos=list(range(p * page + 1, min(p * page + page, P) + 1)),
+                                  ts=0, pinned=True, slot=p))
+            per_step = []
+            for i in range(stream.T):
+                t = P + i + 1
+                cur = max(pages, key=lambda pg: pg["pos"][-1]) if pages else None
+                ev = -1
+                if cur is not None and len(cur["pos"]) < page:
+                    tgt = cur
+                else:
+                    if len(pages) < C:
+                        tgt = dict(pos=[], ts=0, pinned=False, slot=len(pages))
+                        pages.append(tgt)
+                    else:
+                        victim = min((pg for pg in pages if not pg["pinned"]),
+                                     key=lambda pg: (pg["ts"], pg["pos"][0]))
+                        ev = victim["pos"][0]
+                        victim.update(pos=[], pinned=False)
+                        tgt = victim
+                tgt["pos"].append(t)
+                if not tgt["pinned"]:
+                    tgt["ts"] = t
+                q = bf16_to_f32(stream.q[i, b]).astype(np.float64)
+                allpos = sorted(x for pg in pages for x in pg["pos"])
+                idx = np.array(allpos) - 1
+                outs, probs = [], []
+                for j in range(g):
+                    s = scale * (K[b, kv, idx] @ q[kv * g + j])
+                    e = np.exp(s)
+                    pr = e / e.sum()
+                    outs.append(pr @ V[b, kv, idx])
+                    probs.append(dict(zip(allpos, pr)))
+                for pg in pages:
+                    if not pg["pinned"] and any(pr[x] > alpha for pr in probs for x in pg["pos"]):
+                        pg["ts"] = t
+                margin = min(abs(pr[x] - alpha) for pr in probs for x in allpos)
+                snap = sorted((pg["slot"], pg["pos"][0], len(pg["pos"]), pg["ts"]) for pg in pages)
+                per_step.append((snap, ev, np.array(outs), margin))
+            res.append(per_step)
+    return res
+
+
+@pytest.mark.parametrize("page,L,P,g,alpha", [(1, 6, 2, 1, 0.12), (2, 6, 2, 2, 0.08), (1, 5, 1, 3, 0.15),
+                                              (2, 8, 3, 1, 0.1)])
+def test_p6_brute_force_end_to_end(oracle_mod, page, L, P, g, alpha):
+    B, Hkv, d, T = 2, 2, 4, 8
+    st = gaussian_stream(100 + page * 10 + L, B, g * Hkv, Hkv, d, P, T, sigma_q=2.0)
+    ref = brute_force_end_to_end(st, L, alpha, page, g)
+    got = []
+
+    def on_step(i, t, o, out):
+        got.append((o.get_state(), o.get_trace()["evicted"].copy(), out.copy()))
+
+    run_oracle(oracle_mod, st, L=L, alpha=alpha, page=page, Hq=g * Hkv, Hkv=Hkv, on_step=on_step)
+    n_mixed = 0
+    for u in range(B * Hkv):
+        b, kv = divmod(u, Hkv)
+        for i in range(T):
+            snap, ev, outs, margin = ref[u][i]
+            assert margin > 1e-9, "borderline draw; change the seed"
+            state, evs, out = got[i]
+            mine = sorted((p, int(state["start"][u, p]), int(state["count"][u, p]),
+                           int(state["ts"][u, p])) for p in range(L // page) if state["count"][u, p] > 0)
+            assert mine == snap, (u, i)
+            assert evs[u] == ev
+            assert np.abs(out[b, kv * g:(kv + 1) * g] - outs).max() < 1e-12
+            n_mixed += ev >= 0
+    assert n_mixed > 0
+
+
+# ---------------------------------------------------------------- errors
+
+
+def test_oracle_error_codes(oracle_mod):
+    O = oracle_mod.Oracle
+    with pytest.raises(oracle_mod.OracleError):
+        O(L=50, alpha=1e-4, page=16, n_q_heads=4, n_kv_heads=2, head_dim=8, batch=1)   # L % page
+    with pytest.raises(oracle_mod.OracleError):
+        O(L=64, alpha=1e-4, page=16, n_q_heads=3, n_kv_heads=2, head_dim=8, batch=1)   # Hq % Hkv
+    o = O(L=64, alpha=1e-4, page=16, n_q_heads=2, n_kv_heads=1, head_dim=8, batch=1)
+    z = np.zeros((1, 2, 8), np.uint16)
+    with pytest.raises(oracle_mod.OracleError) as e:
+        o.decode_step(z, z[:, :1], z[:, :1])                                            # before prefill
+    assert e.value.code == oracle_mod.REF_E_STATE
+    kp = np.zeros((1, 1, 49, 8), np.uint16)
+    with pytest.raises(oracle_mod.OracleError) as e:
+        o.prefill(kp, kp, 49)                                                           # D14 budget
+    assert e.value.code == oracle_mod.REF_E_BUDGET
+    o.prefill(kp[:, :, :48], kp[:, :, :48], 48)
+    with pytest.raises(oracle_mod.OracleError) as e:
+        o.prefill(kp[:, :, :48], kp[:, :, :48], 48)                                     # twice
+    assert e.value.code == oracle_mod.REF_E_STATE
+
+
+def test_d3_strict_threshold(oracle_mod):
+    """D3: "above" alpha (:29), "exceeds" (:100), "exceeding" (:364) -> strict '>'.
+    With q = 0 every resident token has p = 1/n exactly; with n = 4 and alpha = 1/4 the
+    two unpinned, not-just-written tokens sit exactly on the threshold and must NOT be
+    stamped (their timestamps stay at their write times)."""
+    d = 8
+    o = oracle_mod.Oracle(L=8, alpha=0.25, page=1, n_q_heads=1, n_kv_heads=1, head_dim=d, batch=1)
+    rng = np.random.default_rng(0)
+    from paper_2502_11147_b200.synth import bf16_bits
+    kv = lambda *s: bf16_bits(rng.standard_normal(s).astype(np.float32))
+    o.prefill(kv(1, 1, 1, d), kv(1, 1, 1, d), 1)
+    zero_q = np.zeros((1, 1, d), np.uint16)
+    for _ in range(3):                      # t = 2, 3, 4
+        o.decode_step(zero_q, kv(1, 1, d), kv(1, 1, d))
+    st = o.get_state()
+    ts = {int(s): int(t) for s, t, c in zip(st["start"][0], st["ts"][0], st["count"][0]) if c}
+    assert ts == {1: 0, 2: 2, 3: 3, 4: 4}
+    o.close()
+    o = oracle_mod.Oracle(L=8, alpha=0.2499, page=1, n_q_heads=1, n_kv_heads=1, head_dim=d, batch=1)
+    o.prefill(kv(1, 1, 1, d), kv(1, 1, 1, d), 1)
+    for _ in range(3):
+        o.decode_step(zero_q, kv(1, 1, d), kv(1, 1, d))
+    st = o.get_state()
+    ts = {int(s): int(t) for s, t, c in zip(st["start"][0], st["ts"][0], st["count"][0]) if c}
+    assert ts == {1: 0, 2: 4, 3: 4, 4: 4}
