@@ -431,7 +431,7 @@ def test_d3_strict_threshold(oracle_mod):
         o.decode_step(zero_q, kv(1, 1, d), kv(1, 1, d))
     st = o.get_state()
     ts = {int(s): int(t) for s, t, c in zip(st["start"][0], st["ts"][0], st["count"][0]) if c}
-    assert ts == {1: 0, 2: 2, 3: 3, 4: 4}
+    assert ts == {1: 0, 2: 3, 3: 3, 4: 4}    # t=3: p=1/3 > 1/4 stamps 2; t=4: p=1/4 stamps nothing
     o.close()
     o = oracle_mod.Oracle(L=8, alpha=0.2499, page=1, n_q_heads=1, n_kv_heads=1, head_dim=d, batch=1)
     o.prefill(kv(1, 1, 1, d), kv(1, 1, 1, d), 1)
