@@ -1,0 +1,490 @@
+// raas_api.cu — host side of libraas: config validation, arena carving, TMA descriptors,
+// launches.  The C ABI is declared (and documented, with citations) in include/raas.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/raas.h"
+#include "raas_kernels.cuh"
+
+using raas::DecodeParams;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define RAAS_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(RAAS_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));           \
+  } while (0)
+
+constexpr size_t ALIGN = 1024;
+size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+// decode kernel shape (tuned on B200)
+constexpr int NW = 4;      // warps per CTA (each an independent worker)
+constexpr int STAGES = 3;  // pages in flight per warp
+
+template <int D>
+constexpr int smem_bytes() {
+  return 1024 + NW * STAGES * (2 * raas::PAGE * D * 2) + NW * STAGES * (8 + 32);
+}
+
+struct Layout {
+  size_t kstore, vstore, ts, start, cnt, npin, plan, counter, pmax, part_acc, part_ml, status,
+      stats, sq, sk, sv, so, total;
+};
+
+struct Derived {
+  int C, units, g, split_pages, nsplit;
+};
+
+int derive(const raas_config* c, Derived* d) {
+  if (!c) return fail(RAAS_E_INVALID, "null config");
+  if (c->L <= 0 || c->page <= 0 || c->n_q_heads <= 0 || c->n_kv_heads <= 0 ||
+      c->head_dim <= 0 || c->batch <= 0)
+    return fail(RAAS_E_INVALID, "non-positive size in config");
+  if (c->L % c->page != 0) return fail(RAAS_E_INVALID, "L %% page != 0");
+  if (c->n_q_heads % c->n_kv_heads != 0) return fail(RAAS_E_INVALID, "n_q_heads %% n_kv_heads != 0");
+  if (!(c->alpha >= 0.f)) return fail(RAAS_E_INVALID, "alpha must be >= 0");
+  if (c->softmax_scale < 0.f) return fail(RAAS_E_INVALID, "softmax_scale must be >= 0");
+  if (c->page != raas::PAGE) return fail(RAAS_E_UNSUPPORTED, "page must be 16");
+  if (c->head_dim != 64 && c->head_dim != 128)
+    return fail(RAAS_E_UNSUPPORTED, "head_dim must be 64 or 128");
+  d->g = c->n_q_heads / c->n_kv_heads;
+  if (d->g > raas::MAX_GROUP) return fail(RAAS_E_UNSUPPORTED, "GQA group > 8");
+  d->C = c->L / c->page;
+  d->units = c->batch * c->n_kv_heads;
+  if ((long long)d->units * d->C * raas::PAGE >= (1LL << 31))
+    return fail(RAAS_E_UNSUPPORTED, "units * L too large for 32-bit TMA row coordinates");
+  int sp = c->split_pages > 0 ? c->split_pages : 8;
+  if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "split_pages must be <= 32");
+  const int min_sp = (d->C + raas::MAX_SPLITS - 1) / raas::MAX_SPLITS;
+  if (sp < min_sp) sp = min_sp;
+  if (sp > d->C) sp = d->C;
+  if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "L too large (more than 32*32 pages)");
+  d->split_pages = sp;
+  d->nsplit = (d->C + sp - 1) / sp;
+  return RAAS_OK;
+}
+
+Layout layout(const raas_config* c, const Derived& d) {
+  Layout L{};
+  const size_t U = d.units, C = d.C, D = c->head_dim, g = d.g;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = up(o + bytes); return r; };
+  L.kstore = take(U * C * raas::PAGE * D * 2);
+  L.vstore = take(U * C * raas::PAGE * D * 2);
+  L.ts = take(U * C * 4);
+  L.start = take(U * C * 4);
+  L.cnt = take(U * C * 4);
+  L.npin = take(U * 4);
+  L.plan = take(U * 16);
+  L.counter = take(U * 4);
+  L.pmax = take(U * C * g * 4);
+  L.part_acc = take(U * d.nsplit * g * D * 4);
+  L.part_ml = take(U * d.nsplit * g * 8);
+  L.status = take(16);
+  L.stats = take(64);
+  L.sq = take(U * g * D * 2);
+  L.sk = take(U * D * 2);
+  L.sv = take(U * D * 2);
+  L.so = take(U * g * D * 2);
+  L.total = o;
+  return L;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+struct raas_handle {
+  raas_config cfg;
+  Derived d;
+  Layout lay;
+  int device;
+  int num_sms;
+  int grid;
+  int smem;
+  uint8_t* arena;
+  int prefilled;
+  CUtensorMap tmK, tmV;
+};
+
+namespace {
+
+template <int D>
+int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* v_new,
+                  void* out, cudaStream_t st) {
+  DecodeParams p{};
+  uint8_t* a = h->arena;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.kstore = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kstore);
+  p.vstore = reinterpret_cast<__nv_bfloat16*>(a + h->lay.vstore);
+  p.ts = reinterpret_cast<int32_t*>(a + h->lay.ts);
+  p.start = reinterpret_cast<int32_t*>(a + h->lay.start);
+  p.cnt = reinterpret_cast<int32_t*>(a + h->lay.cnt);
+  p.npin = reinterpret_cast<const int32_t*>(a + h->lay.npin);
+  p.plan = reinterpret_cast<int4*>(a + h->lay.plan);
+  p.counter = reinterpret_cast<int32_t*>(a + h->lay.counter);
+  p.pmax = reinterpret_cast<float*>(a + h->lay.pmax);
+  p.part_acc = reinterpret_cast<float*>(a + h->lay.part_acc);
+  p.part_ml = reinterpret_cast<float2*>(a + h->lay.part_ml);
+  p.status = reinterpret_cast<uint32_t*>(a + h->lay.status);
+  p.stats = reinterpret_cast<unsigned long long*>(a + h->lay.stats);
+  p.units = h->d.units;
+  p.C = h->d.C;
+  p.nsplit = h->d.nsplit;
+  p.split_pages = h->d.split_pages;
+  p.g = h->d.g;
+  const float scale = h->cfg.softmax_scale > 0.f ? h->cfg.softmax_scale
+                                                 : 1.0f / sqrtf((float)h->cfg.head_dim);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.log2_alpha = h->cfg.alpha > 0.f ? log2f(h->cfg.alpha) : -INFINITY;
+
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(h->grid);
+  lc.blockDim = dim3(NW * 32);
+  lc.dynamicSmemBytes = h->smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  RAAS_CUDA(cudaLaunchKernelEx(&lc, raas::raas_decode_kernel<D, NW, STAGES>, p, h->tmK, h->tmV));
+  return RAAS_OK;
+}
+
+template <int D>
+int setup_kernel(raas_handle* h) {
+  auto k = raas::raas_decode_kernel<D, NW, STAGES>;
+  h->smem = smem_bytes<D>();
+  RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
+  int per_sm = 0;
+  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, h->smem));
+  if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
+  const long long tiles = (long long)h->d.units * h->d.nsplit;
+  const long long need = (tiles + NW - 1) / NW;
+  const long long cap = (long long)h->num_sms * per_sm;
+  h->grid = (int)(need < cap ? need : cap);
+  return RAAS_OK;
+}
+
+int make_tmap(raas_handle* h, CUtensorMap* m, void* base) {
+  auto enc = get_encode();
+  if (!enc) return fail(RAAS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t D = h->cfg.head_dim;
+  const cuuint64_t rows = (cuuint64_t)h->d.units * h->d.C * raas::PAGE;
+  cuuint64_t gdim[2] = {D, rows};
+  cuuint64_t gstride[1] = {D * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)raas::PAGE};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RAAS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RAAS_OK;
+}
+
+int refresh(raas_handle* h, cudaStream_t st) {
+  uint8_t* a = h->arena;
+  const int wpb = 4;
+  raas::raas_refresh<<<(h->d.units + wpb - 1) / wpb, 32 * wpb, 0, st>>>(
+      reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
+      reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
+      reinterpret_cast<int4*>(a + h->lay.plan), reinterpret_cast<int32_t*>(a + h->lay.counter),
+      reinterpret_cast<uint32_t*>(a + h->lay.status), h->d.units, h->d.C);
+  RAAS_CUDA(cudaGetLastError());
+  return RAAS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* raas_last_error(void) { return g_err; }
+
+size_t raas_arena_bytes(const raas_config* cfg) {
+  Derived d;
+  if (derive(cfg, &d) != RAAS_OK) return 0;
+  return layout(cfg, d).total;
+}
+
+int raas_create(const raas_config* cfg, void* arena, size_t arena_bytes, int device,
+                raas_handle** out) {
+  if (!out) return fail(RAAS_E_INVALID, "null output handle");
+  *out = nullptr;
+  Derived d;
+  int rc = derive(cfg, &d);
+  if (rc) return rc;
+  Layout lay = layout(cfg, d);
+  if (!arena || (reinterpret_cast<uintptr_t>(arena) & (ALIGN - 1)) != 0)
+    return fail(RAAS_E_ARENA, "arena must be a 1024-byte aligned device pointer");
+  if (arena_bytes < lay.total)
+    return fail(RAAS_E_ARENA, "arena too small: %zu < %zu", arena_bytes, lay.total);
+  DeviceGuard guard(device);
+  raas_handle* h = new raas_handle();
+  h->cfg = *cfg;
+  h->d = d;
+  h->lay = lay;
+  h->device = device;
+  h->arena = static_cast<uint8_t*>(arena);
+  int sms = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(RAAS_E_CUDA, "cudaDeviceGetAttribute: %s", cudaGetErrorString(e));
+  }
+  h->num_sms = sms;
+  rc = cfg->head_dim == 128 ? setup_kernel<128>(h) : setup_kernel<64>(h);
+  if (!rc) rc = make_tmap(h, &h->tmK, h->arena + lay.kstore);
+  if (!rc) rc = make_tmap(h, &h->tmV, h->arena + lay.vstore);
+  if (!rc) {
+    e = cudaMemset(arena, 0, lay.total);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = fail(RAAS_E_CUDA, "arena memset: %s", cudaGetErrorString(e));
+  }
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return RAAS_OK;
+}
+
+int raas_destroy(raas_handle* h) {
+  delete h;
+  return RAAS_OK;
+}
+
+int raas_prefill(raas_handle* h, const void* k, const void* v, int32_t P, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  if (h->prefilled) return fail(RAAS_E_STATE, "handle already prefilled");
+  if (P < 0) return fail(RAAS_E_INVALID, "P < 0");
+  const int Pp = (P + raas::PAGE - 1) / raas::PAGE;
+  if (Pp >= h->d.C) return fail(RAAS_E_BUDGET, "ceil(P/16)=%d leaves no decode page (C=%d)", Pp, h->d.C);
+  if (P > 0 && (!k || !v || !aligned16(k) || !aligned16(v)))
+    return fail(RAAS_E_INVALID, "k/v must be non-null 16-byte aligned device pointers");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* a = h->arena;
+  auto* ks = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kstore);
+  auto* vs = reinterpret_cast<__nv_bfloat16*>(a + h->lay.vstore);
+  if (P > 0) {
+    const size_t total = (size_t)h->d.units * P * (h->cfg.head_dim / 8);
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)h->num_sms * 16);
+    if (h->cfg.head_dim == 128)
+      raas::raas_prefill_copy<128><<<blocks, 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), ks, vs,
+          h->d.units, P, h->d.C);
+    else
+      raas::raas_prefill_copy<64><<<blocks, 256, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), ks, vs,
+          h->d.units, P, h->d.C);
+    RAAS_CUDA(cudaGetLastError());
+  }
+  const size_t n = (size_t)h->d.units * h->d.C;
+  raas::raas_meta_init<<<(int)std::min<size_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+      reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
+      reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
+      reinterpret_cast<int4*>(a + h->lay.plan), h->d.units, h->d.C, P);
+  RAAS_CUDA(cudaGetLastError());
+  int rc = refresh(h, st);
+  if (rc) return rc;
+  h->prefilled = 1;
+  return RAAS_OK;
+}
+
+int raas_decode_step(raas_handle* h, const void* q, const void* k_new, const void* v_new,
+                     void* out, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  if (!h->prefilled) return fail(RAAS_E_STATE, "decode before prefill");
+  if (!q || !k_new || !v_new || !out || !aligned16(q) || !aligned16(k_new) ||
+      !aligned16(v_new) || !aligned16(out))
+    return fail(RAAS_E_INVALID, "q/k_new/v_new/out must be non-null 16-byte aligned device pointers");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return h->cfg.head_dim == 128 ? launch_decode<128>(h, q, k_new, v_new, out, st)
+                                : launch_decode<64>(h, q, k_new, v_new, out, st);
+}
+
+int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_host,
+                          const void* v_new_host, void* out_host, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  if (!h->prefilled) return fail(RAAS_E_STATE, "decode before prefill");
+  if (!q_host || !k_new_host || !v_new_host || !out_host)
+    return fail(RAAS_E_INVALID, "null host buffer");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* a = h->arena;
+  const size_t D = h->cfg.head_dim, U = h->d.units, g = h->d.g;
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sq, q_host, U * g * D * 2, cudaMemcpyHostToDevice, st));
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sk, k_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sv, v_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
+  int rc = h->cfg.head_dim == 128
+               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, a + h->lay.so, st)
+               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, a + h->lay.so, st);
+  if (rc) return rc;
+  RAAS_CUDA(cudaMemcpyAsync(out_host, a + h->lay.so, U * g * D * 2, cudaMemcpyDeviceToHost, st));
+  return RAAS_OK;
+}
+
+int raas_get_state(raas_handle* h, int32_t* t, int32_t* ts, int32_t* start_pos, int32_t* count,
+                   uint8_t* pinned, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t U = h->d.units, C = h->d.C;
+  std::vector<int32_t> npin(U), vts(U * C);
+  std::vector<int4> plan(U);
+  uint8_t* a = h->arena;
+  RAAS_CUDA(cudaMemcpyAsync(npin.data(), a + h->lay.npin, U * 4, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaMemcpyAsync(plan.data(), a + h->lay.plan, U * 16, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaMemcpyAsync(vts.data(), a + h->lay.ts, U * C * 4, cudaMemcpyDeviceToHost, st));
+  if (start_pos)
+    RAAS_CUDA(cudaMemcpyAsync(start_pos, a + h->lay.start, U * C * 4, cudaMemcpyDeviceToHost, st));
+  if (count)
+    RAAS_CUDA(cudaMemcpyAsync(count, a + h->lay.cnt, U * C * 4, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaStreamSynchronize(st));
+  for (size_t u = 0; u < U; ++u) {
+    if (t) t[u] = plan[u].w - 1;
+    for (size_t p = 0; p < C; ++p) {
+      const bool pin = (int)p < npin[u];
+      if (ts) ts[u * C + p] = pin ? 0 : vts[u * C + p];
+      if (pinned) pinned[u * C + p] = pin ? 1 : 0;
+    }
+  }
+  return RAAS_OK;
+}
+
+int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const int32_t* start_pos,
+                   const int32_t* count, const uint8_t* pinned, const void* k_store_host,
+                   const void* v_store_host, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  if (!t || !ts || !start_pos || !count || !pinned) return fail(RAAS_E_INVALID, "null state array");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t U = h->d.units, C = h->d.C;
+  std::vector<int32_t> npin(U);
+  std::vector<int4> plan(U);
+  for (size_t u = 0; u < U; ++u) {
+    int np = 0;
+    while (np < (int)C && pinned[u * C + np]) ++np;
+    for (size_t p = np; p < C; ++p)
+      if (pinned[u * C + p]) return fail(RAAS_E_INVALID, "pinned pages must be a prefix (unit %zu)", u);
+    bool hole = false;
+    for (size_t p = 0; p < C; ++p) {
+      if (count[u * C + p] < 0 || count[u * C + p] > raas::PAGE)
+        return fail(RAAS_E_INVALID, "count out of range");
+      if (count[u * C + p] == 0) hole = true;
+      else if (hole) return fail(RAAS_E_INVALID, "used pages must be a prefix (unit %zu)", u);
+    }
+    npin[u] = np;
+    plan[u] = make_int4(0, 0, 0, t[u] + 1);
+  }
+  uint8_t* a = h->arena;
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.ts, ts, U * C * 4, cudaMemcpyHostToDevice, st));
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.start, start_pos, U * C * 4, cudaMemcpyHostToDevice, st));
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.cnt, count, U * C * 4, cudaMemcpyHostToDevice, st));
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.npin, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.plan, plan.data(), U * 16, cudaMemcpyHostToDevice, st));
+  const size_t kvb = U * C * raas::PAGE * h->cfg.head_dim * 2;
+  if (k_store_host)
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kstore, k_store_host, kvb, cudaMemcpyHostToDevice, st));
+  if (v_store_host)
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.vstore, v_store_host, kvb, cudaMemcpyHostToDevice, st));
+  int rc = refresh(h, st);
+  if (rc) return rc;
+  RAAS_CUDA(cudaStreamSynchronize(st));
+  h->prefilled = 1;
+  return RAAS_OK;
+}
+
+int raas_get_kv(raas_handle* h, void* k_store_host, void* v_store_host, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t kvb = (size_t)h->d.units * h->d.C * raas::PAGE * h->cfg.head_dim * 2;
+  if (k_store_host)
+    RAAS_CUDA(cudaMemcpyAsync(k_store_host, h->arena + h->lay.kstore, kvb, cudaMemcpyDeviceToHost, st));
+  if (v_store_host)
+    RAAS_CUDA(cudaMemcpyAsync(v_store_host, h->arena + h->lay.vstore, kvb, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaStreamSynchronize(st));
+  return RAAS_OK;
+}
+
+int raas_get_status(raas_handle* h, void* stream) {
+  if (!h) return -fail(RAAS_E_INVALID, "null handle");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t s = 0;
+  if (cudaMemcpyAsync(&s, h->arena + h->lay.status, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return -fail(RAAS_E_CUDA, "status readback failed");
+  return (int)s;
+}
+
+int raas_get_counters(raas_handle* h, uint64_t counters[4], void* stream) {
+  if (!h || !counters) return fail(RAAS_E_INVALID, "null argument");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RAAS_CUDA(cudaMemcpyAsync(counters, h->arena + h->lay.stats, 32, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaStreamSynchronize(st));
+  return RAAS_OK;
+}
+
+int raas_launch_info(const raas_handle* h, int32_t info[5]) {
+  if (!h || !info) return fail(RAAS_E_INVALID, "null argument");
+  info[0] = h->grid;
+  info[1] = NW * 32;
+  info[2] = h->smem;
+  info[3] = h->d.split_pages;
+  info[4] = h->d.nsplit;
+  return RAAS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+"""GPU (libraas) vs CPU oracle lockstep driver (SURVEY.md §8c parity protocol).
+
+After every step: metadata (t, ts, start_pos, count, pinned) must be bit-exact; a differing
+timestamp is tolerated only when the oracle's decisive probability p* of that page lies within
+|p* - alpha| < 1e-6 (a "band event": counted, then the GPU is resynced to the oracle state).
+Outputs are compared against the oracle's fp64 result with max abs error <= 2e-2.
+"""
+import numpy as np
+import torch
+
+from paper_2502_11147_b200.raas import RaasLayer
+from paper_2502_11147_b200.synth import bf16_to_f32
+
+BAND = 1e-6
+OUT_TOL = 2e-2
+
+
+def to_dev(bits, device="cuda"):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(device)
+
+
+def from_dev(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+class LockstepResult:
+    def __init__(self):
+        self.steps = 0
+        self.band_events = 0
+        self.max_err = 0.0
+        self.evictions = 0
+        self.stamp_decisions = 0
+        self.stamps = 0
+        self.gpu_evictions = []   # per step, list of (unit, evicted start_pos)
+
+
+def compare_state(g, o, alpha, pstar, res, layer, resync=True):
+    keys = ("t", "ts", "start", "count", "pinned")
+    same = all(np.array_equal(g[k], o[k]) for k in keys)
+    if same:
+        return
+    # only ts may differ, and only inside the band
+    for k in ("t", "start", "count", "pinned"):
+        assert np.array_equal(g[k], o[k]), f"state field {k} differs outside the stamp band"
+    diff = np.argwhere(g["ts"] != o["ts"])
+    for u, p in diff:
+        ps = pstar[u, p]
+        assert ps >= 0 and abs(ps - alpha) < BAND, (
+            f"ts differs at unit {u} page {p}: gpu {g['ts'][u, p]} oracle {o['ts'][u, p]}, "
+            f"p*={ps!r} outside the |p*-alpha|<{BAND} band")
+        res.band_events += 1
+    if resync:
+        layer.raas_set_state(o["t"], o["ts"], o["start"], o["count"], o["pinned"])
+
+
+def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_every=1,
+                 layer=None, oracle=None, device="cuda", on_step=None):
+    """Drive both sides through the whole stream; returns LockstepResult."""
+    B, _, P, d = stream.k_pre.shape
+    if layer is None:
+        layer = RaasLayer(L, alpha, Hq, Hkv, d, B, device=device, split_pages=split_pages)
+        layer.raas_prefill(to_dev(stream.k_pre, device), to_dev(stream.v_pre, device), P)
+    if oracle is None:
+        oracle = oracle_mod.Oracle(L=L, alpha=alpha, page=16, n_q_heads=Hq, n_kv_heads=Hkv,
+                                   head_dim=d, batch=B)
+        oracle.prefill(stream.k_pre, stream.v_pre, P)
+    res = LockstepResult()
+    out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=device)
+    for i in range(stream.T):
+        q, k, v = (to_dev(x[i], device) for x in (stream.q, stream.k, stream.v))
+        layer.raas_decode_step(q, k, v, out)
+        o_out = oracle.decode_step(stream.q[i], stream.k[i], stream.v[i])
+        res.steps += 1
+        if (i + 1) % check_every and i + 1 != stream.T:
+            continue
+        torch.cuda.synchronize()
+        g_out = bf16_to_f32(from_dev(out)).astype(np.float64)
+        assert np.isfinite(g_out).all()
+        res.max_err = max(res.max_err, float(np.abs(g_out - o_out).max()))
+        g_state = layer.raas_get_state()
+        o_state = oracle.get_state()
+        tr = oracle.get_trace()
+        res.evictions += int((tr["evicted"] >= 0).sum())
+        compare_state(g_state, o_state, alpha, tr["pstar"], res, layer)
+        if on_step is not None:
+            on_step(i, layer, oracle, g_out, o_out)
+    assert layer.raas_get_status() == 0
+    return res, layer, oracle

@@ -1,0 +1,89 @@
+"""CPU checks of the C ABI boundary: libraas.so builds for sm_100a, loads without a GPU,
+exports every function include/raas.h declares, and rejects bad arguments before touching
+the device."""
+import ctypes
+import os
+import shutil
+
+import pytest
+
+from paper_2502_11147_b200 import build as build_mod
+from paper_2502_11147_b200 import raas
+
+HAVE_NVCC = shutil.which("nvcc") is not None or os.path.exists("/usr/local/cuda/bin/nvcc")
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not os.path.exists(raas.LIB_PATH):
+        if not HAVE_NVCC:
+            pytest.skip("no nvcc and no prebuilt libraas.so")
+        build_mod.build()
+    return raas.lib()
+
+
+def test_header_symbols_exported(L):
+    names = raas.header_functions()
+    assert "raas_create" in names and "raas_decode_step" in names and "raas_prefill" in names
+    assert "raas_destroy" in names
+    for n in names:
+        assert hasattr(L, n), f"{n} declared in include/raas.h but not exported"
+    # nothing else named raas_* is exported
+    import subprocess
+
+    out = subprocess.run(["nm", "-D", "--defined-only", raas.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = sorted({ln.split()[-1] for ln in out.splitlines() if " T raas_" in ln})
+    assert exported == names
+
+
+def test_sass_is_sm100a_and_uses_tma_and_tensor_cores(L):
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump) and not shutil.which("cuobjdump"):
+        pytest.skip("no cuobjdump")
+    import subprocess
+
+    sass = subprocess.run([cuobjdump, "-sass", raas.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass
+    assert "UTMALDG" in sass            # TMA tile loads of the KV pages
+    assert "HMMA.16816.F32.BF16" in sass  # bf16 tensor-core MMAs (QK^T and PV)
+    assert "LDSM" in sass and "MOVM" in sass
+
+
+@pytest.mark.parametrize("cfg,expect", [
+    (dict(L=64, alpha=1e-4, n_q_heads=4, n_kv_heads=2, head_dim=64, batch=1), True),
+    (dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=64), True),
+    (dict(L=50, alpha=1e-4, n_q_heads=4, n_kv_heads=2, head_dim=64, batch=1), False),   # L % 16
+    (dict(L=64, alpha=1e-4, n_q_heads=5, n_kv_heads=2, head_dim=64, batch=1), False),   # Hq % Hkv
+    (dict(L=64, alpha=1e-4, n_q_heads=4, n_kv_heads=2, head_dim=96, batch=1), False),   # head_dim
+    (dict(L=64, alpha=1e-4, n_q_heads=32, n_kv_heads=2, head_dim=64, batch=1), False),  # group 16
+    (dict(L=64, alpha=-1.0, n_q_heads=4, n_kv_heads=2, head_dim=64, batch=1), False),   # alpha < 0
+])
+def test_arena_bytes(L, cfg, expect):
+    n = raas.raas_arena_bytes(raas.make_config(**cfg))
+    assert (n > 0) == expect
+    if expect:
+        C, U = cfg["L"] // 16, cfg["batch"] * cfg["n_kv_heads"]
+        kv = 2 * U * C * 16 * cfg["head_dim"] * 2
+        assert kv <= n <= kv * 1.2 + (1 << 20)   # O(L): the KV store dominates
+
+
+def test_arena_is_linear_in_L_not_N(L):
+    """Memory plateaus at the budget (PAPER.md :191-193): the arena depends on L only."""
+    a = [raas.raas_arena_bytes(raas.make_config(L=L_, alpha=1e-4, n_q_heads=32, n_kv_heads=8,
+                                                head_dim=128, batch=4)) for L_ in (512, 1024, 2048)]
+    assert a[1] - a[0] == pytest.approx(a[2] - a[1], rel=0.02) or a[2] - a[1] == pytest.approx(2 * (a[1] - a[0]), rel=0.05)
+
+
+def test_create_rejects_bad_args_without_gpu(L):
+    cfg = raas.make_config(L=64, alpha=1e-4, n_q_heads=4, n_kv_heads=2, head_dim=64, batch=1)
+    h = ctypes.c_void_p()
+    n = raas.raas_arena_bytes(cfg)
+    assert L.raas_create(ctypes.byref(cfg), ctypes.c_void_p(1024), n - 1, 0, ctypes.byref(h)) == raas.RAAS_E_ARENA
+    assert L.raas_create(ctypes.byref(cfg), ctypes.c_void_p(1025), n, 0, ctypes.byref(h)) == raas.RAAS_E_ARENA
+    assert L.raas_create(ctypes.byref(cfg), None, n, 0, ctypes.byref(h)) == raas.RAAS_E_ARENA
+    bad = raas.make_config(L=64, alpha=1e-4, n_q_heads=4, n_kv_heads=2, head_dim=80, batch=1)
+    assert L.raas_create(ctypes.byref(bad), ctypes.c_void_p(1024), 1 << 30, 0, ctypes.byref(h)) == raas.RAAS_E_UNSUPPORTED
+    assert b"head_dim" in L.raas_last_error()
+    assert L.raas_decode_step(None, None, None, None, None, None) == raas.RAAS_E_INVALID
+    assert L.raas_prefill(None, None, None, 0, None) == raas.RAAS_E_INVALID

@@ -1,0 +1,294 @@
+"""GPU parity: libraas (hand-written sm_100a CUDA through the C ABI) vs the fp64 CPU oracle.
+
+Bar (BASELINE.json north_star): occupancy, timestamps and eviction order bit-exact; a
+differing stamp decision only where |p* - alpha| < 1e-6, counted (0 on this test set);
+attention output within max abs error 2e-2 (bf16 K/V, fp32 accumulation)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from lockstep import OUT_TOL, from_dev, run_lockstep, to_dev  # noqa: E402
+from paper_2502_11147_b200.raas import RAAS_E_BUDGET, RAAS_E_STATE, RaasError, RaasLayer  # noqa: E402
+from paper_2502_11147_b200.synth import (bf16_bits, bf16_to_f32, gaussian_stream,  # noqa: E402
+                                         random_steady_state, waterfall_stream)
+from traces import page_twin_stream  # noqa: E402
+
+PAGE = 16
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2502_11147_b200 import build, raas
+
+    build.build()
+    raas.lib()
+
+
+# ------------------------------------------------------------------ config 1 (toy), full run
+
+
+def test_toy_config_full_run_lockstep(oracle_mod):
+    """BASELINE.json configs[0]: 1 layer, 1 request, 4q/2kv, d=64, prefill 32, 256 decode
+    steps, L=64, alpha=1e-4 — free-running, compared after every step."""
+    st = waterfall_stream(1000, 1, 4, 2, 64, 32, 256, lam=6.0)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=64, alpha=1e-4, Hq=4, Hkv=2)
+    assert res.band_events == 0
+    assert res.max_err <= OUT_TOL
+    assert res.evictions > 0
+    c = layer.raas_get_counters()
+    assert c["unit_steps"] == 256 * 2 and 0 < c["stamps"] < c["decisions"]
+
+
+def test_page_twin_hand_trace_on_gpu(oracle_mod):
+    """P3' (tests/golden/p3_page_twin.json): the hand-derived page evictions reproduce."""
+    for gh in (1, 4, 8):
+        g, st = page_twin_stream(g_heads=gh, value_seed=5)
+        s, exp = g["setup"], g["expected"]
+        evs = []
+
+        def on_step(i, layer, oracle, g_out, o_out):
+            ev = oracle.get_trace()["evicted"][0]
+            if ev >= 0:
+                evs.append([s["P"] + i + 1, (int(ev) - 1) // PAGE + 1])
+
+        res, layer, _ = run_lockstep(oracle_mod, st, L=s["L"], alpha=s["alpha"], Hq=gh, Hkv=1,
+                                     on_step=on_step)
+        assert evs == exp["page_evictions"]
+        gs = layer.raas_get_state()
+        pages = sorted((int(x) - 1) // PAGE + 1 for x in gs["start"][0])
+        assert pages == exp["final_pages"]
+        ts = {(int(x) - 1) // PAGE + 1: int(t) for x, t, pn in
+              zip(gs["start"][0], gs["ts"][0], gs["pinned"][0]) if not pn}
+        assert ts == {int(k): v for k, v in exp["final_ts"].items()}
+        assert res.band_events == 0
+
+
+# ------------------------------------------------------------------ random small configs
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,lam", [
+    (3, 8, 2, 128, 40, 300, 256, 0, 6.0),     # Llama-like group 4, partial pinned page
+    (2, 28, 4, 128, 128, 200, 512, 0, 6.0),   # Qwen-like group 7
+    (2, 4, 4, 64, 17, 250, 128, 0, 5.0),      # group 1
+    (1, 16, 2, 128, 0, 220, 128, 0, 6.0),     # group 8, no prompt at all
+    (2, 8, 2, 128, 64, 200, 384, 3, 6.0),     # ragged split tail (24 pages / 3)
+    (2, 8, 2, 64, 100, 180, 160, 1, 4.0),     # one page per split
+    (1, 8, 1, 128, 33, 260, 64, 0, 8.0),      # 4 pages: C - Pp = 1 (current page is the victim)
+])
+def test_random_configs_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, lam):
+    st = waterfall_stream(7 + B + Hq + P, B, Hq, Hkv, d, P, T, lam=lam)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, split_pages=sp)
+    assert res.band_events == 0
+    assert res.max_err <= OUT_TOL
+    if P + T > L:
+        assert res.evictions > 0
+
+
+@pytest.mark.parametrize("alpha", [0.0, 1.0])
+def test_alpha_extremes_sliding_window(oracle_mod, alpha):
+    """P4 on the GPU: alpha=0 stamps everything, alpha>=1 nothing — both StreamingLLM-like."""
+    st = gaussian_stream(3, 2, 8, 2, 128, 100, 200)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=128, alpha=alpha, Hq=8, Hkv=2)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL
+
+
+def test_dense_equivalence_gpu():
+    """P1 on the GPU: with L >= N nothing is evicted and out == textbook attention."""
+    B, Hq, Hkv, d, P, T = 2, 8, 2, 128, 50, 60
+    st = gaussian_stream(9, B, Hq, Hkv, d, P, T)
+    L = 128
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+    K = np.concatenate([bf16_to_f32(st.k_pre), np.moveaxis(bf16_to_f32(st.k), 0, 2)], 2).astype(np.float64)
+    V = np.concatenate([bf16_to_f32(st.v_pre), np.moveaxis(bf16_to_f32(st.v), 0, 2)], 2).astype(np.float64)
+    out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
+    worst = 0.0
+    for i in range(T):
+        layer.raas_decode_step(to_dev(st.q[i]), to_dev(st.k[i]), to_dev(st.v[i]), out)
+        torch.cuda.synchronize()
+        g = bf16_to_f32(from_dev(out)).astype(np.float64)
+        q = bf16_to_f32(st.q[i]).astype(np.float64)
+        n = P + i + 1
+        for b in range(B):
+            for h in range(Hq):
+                s = (K[b, h // 4, :n] @ q[b, h]) / math.sqrt(d)
+                w = np.exp(s - s.max())
+                ref = (w / w.sum()) @ V[b, h // 4, :n]
+                worst = max(worst, np.abs(ref - g[b, h]).max())
+    assert worst <= OUT_TOL
+    assert layer.raas_get_counters()["evictions"] == 0
+
+
+# ------------------------------------------------------------------ determinism / sharding
+
+
+def _run_gpu(st, L, Hq, Hkv, batch_slice=None, split_pages=0):
+    B, _, P, d = st.k_pre.shape
+    sl = batch_slice if batch_slice is not None else slice(0, B)
+    kp, vp = st.k_pre[sl], st.v_pre[sl]
+    Bs = kp.shape[0]
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, Bs, split_pages=split_pages)
+    layer.raas_prefill(to_dev(kp), to_dev(vp), P)
+    out = torch.empty((Bs, Hq, d), dtype=torch.bfloat16, device="cuda")
+    outs = []
+    for i in range(st.T):
+        layer.raas_decode_step(to_dev(st.q[i][sl]), to_dev(st.k[i][sl]), to_dev(st.v[i][sl]), out)
+        outs.append(from_dev(out))
+    return np.stack(outs), layer.raas_get_state()
+
+
+def test_bitwise_determinism_and_request_sharding():
+    """Run-to-run bitwise determinism, and results of a request shard (G=2 split of the
+    batch) bitwise identical to the unsharded run (split size independent of batch)."""
+    st = waterfall_stream(21, 4, 8, 2, 128, 48, 150)
+    a, sa = _run_gpu(st, 256, 8, 2)
+    b, sb = _run_gpu(st, 256, 8, 2)
+    assert np.array_equal(a, b) and all(np.array_equal(sa[k], sb[k]) for k in sa)
+    lo, slo = _run_gpu(st, 256, 8, 2, slice(0, 2))
+    hi, shi = _run_gpu(st, 256, 8, 2, slice(2, 4))
+    assert np.array_equal(np.concatenate([lo, hi], axis=1), a)
+    for k in ("ts", "start", "count"):
+        assert np.array_equal(np.concatenate([slo[k], shi[k]]), sa[k])
+
+
+def test_host_entry_point_matches_device_entry_point():
+    B, Hq, Hkv, d, P, T, L = 2, 8, 2, 128, 40, 40, 64
+    st = waterfall_stream(4, B, Hq, Hkv, d, P, T)
+    dev, _ = _run_gpu(st, L, Hq, Hkv)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+    out_h = torch.empty((B, Hq, d), dtype=torch.bfloat16).pin_memory()
+    outs = []
+    for i in range(T):
+        qh = torch.from_numpy(st.q[i].view(np.int16)).view(torch.bfloat16).pin_memory()
+        kh = torch.from_numpy(st.k[i].view(np.int16)).view(torch.bfloat16).pin_memory()
+        vh = torch.from_numpy(st.v[i].view(np.int16)).view(torch.bfloat16).pin_memory()
+        layer.raas_decode_step_host(qh, kh, vh, out_h)
+        torch.cuda.current_stream().synchronize()
+        outs.append(out_h.view(torch.int16).numpy().view(np.uint16).copy())
+    assert np.array_equal(np.stack(outs), dev)
+
+
+def test_cuda_graph_capture_matches_eager():
+    """decode_step is graph-capturable (no host sync; cursor and victim on the device)."""
+    B, Hq, Hkv, d, P, T, L = 2, 8, 2, 128, 40, 96, 96
+    st = waterfall_stream(8, B, Hq, Hkv, d, P, T)
+    eager, s_e = _run_gpu(st, L, Hq, Hkv)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+    torch.cuda.synchronize()
+    qs = [to_dev(x) for x in st.q]
+    ks = [to_dev(x) for x in st.k]
+    vs = [to_dev(x) for x in st.v]
+    outs = [torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda") for _ in range(T)]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(T):
+            layer.raas_decode_step(qs[i], ks[i], vs[i], outs[i], stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    got = np.stack([from_dev(o) for o in outs])
+    assert np.array_equal(got, eager)
+    s_g = layer.raas_get_state()
+    assert all(np.array_equal(s_g[k], s_e[k]) for k in s_e)
+
+
+def test_no_device_allocation_after_create():
+    """O(L) memory (PAPER.md :191-193): decode steps allocate nothing."""
+    B, Hq, Hkv, d, P, L = 4, 32, 8, 128, 64, 256
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    k = torch.randn(B, Hkv, P, d, device="cuda").bfloat16()
+    layer.raas_prefill(k, k.clone(), P)
+    q = torch.randn(B, Hq, d, device="cuda").bfloat16()
+    kn = torch.randn(B, Hkv, d, device="cuda").bfloat16()
+    out = torch.empty_like(q)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(400):
+        layer.raas_decode_step(q, kn, kn, out)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 == free1
+    assert layer.raas_get_counters()["evictions"] > 0
+
+
+def test_error_codes_gpu():
+    layer = RaasLayer(64, 1e-4, 4, 2, 64, 1)
+    q = torch.zeros(1, 4, 64, dtype=torch.bfloat16, device="cuda")
+    kv = torch.zeros(1, 2, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(RaasError) as e:
+        layer.raas_decode_step(q, kv, kv, q.clone())
+    assert e.value.code == RAAS_E_STATE
+    big = torch.zeros(1, 2, 64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(RaasError) as e:
+        layer.raas_prefill(big, big, 64)           # ceil(64/16) = 4 = C: no decode page (D14)
+    assert e.value.code == RAAS_E_BUDGET
+    layer.raas_prefill(big[:, :, :48].contiguous(), big[:, :, :48].contiguous(), 48)
+    with pytest.raises(RaasError) as e:
+        layer.raas_prefill(big[:, :, :48].contiguous(), big[:, :, :48].contiguous(), 48)
+    assert e.value.code == RAAS_E_STATE
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,L,P", [(64, 32, 8, 2048, 256), (32, 28, 4, 4096, 128)])
+def test_full_size_sampled_units_lockstep(oracle_mod, B, Hq, Hkv, L, P):
+    """BASELINE.json configs[2] / [3] shapes in the launch configuration bench.py times:
+    the whole batch runs on the GPU from a full-cache state; the first and last request
+    (all kv-heads) are replayed on the oracle in lockstep with resync."""
+    d, T = 128, 24
+    C, Pp = L // PAGE, -(-P // PAGE)
+    U = B * Hkv
+    t_now = Pp * PAGE + 4 * PAGE * (C - Pp) + 5
+    meta = random_steady_state(77, U, C, Pp, t_now)
+    rng = np.random.Generator(np.random.Philox(78))
+    kst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
+    vst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"], kst, vst)
+    sample = [0, B - 1]
+    units = [b * Hkv + h for b in sample for h in range(Hkv)]
+    orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
+                            batch=len(sample))
+    orc.set_state(meta["t"][units], meta["ts"][units], meta["start"][units], meta["count"][units],
+                  meta["pinned"][units], kst[units], vst[units])
+    g = Hq // Hkv
+    band = 0
+    worst = 0.0
+    out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
+    for i in range(T):
+        # queries aimed at a few pages so stamping is selective
+        q = 2.5 * rng.standard_normal((B, Hq, d), np.float32)
+        qb, kb, vb = bf16_bits(q), bf16_bits(rng.standard_normal((B, Hkv, d), np.float32)), \
+            bf16_bits(rng.standard_normal((B, Hkv, d), np.float32))
+        layer.raas_decode_step(to_dev(qb), to_dev(kb), to_dev(vb), out)
+        o_out = orc.decode_step(qb[sample], kb[sample], vb[sample])
+        gs = layer.raas_get_state()
+        os_ = orc.get_state()
+        tr = orc.get_trace()
+        g_out = bf16_to_f32(from_dev(out)).astype(np.float64)[sample]
+        worst = max(worst, np.abs(g_out - o_out).max())
+        for k in ("t", "start", "count", "pinned"):
+            assert np.array_equal(gs[k][units], os_[k])
+        diff = np.argwhere(gs["ts"][units] != os_["ts"])
+        for u, p in diff:
+            assert abs(tr["pstar"][u, p] - 1e-4) < 1e-6
+            band += 1
+        if len(diff):
+            full = {k: gs[k].copy() for k in gs}
+            for j, u in enumerate(units):
+                full["ts"][u] = os_["ts"][j]
+            layer.raas_set_state(full["t"], full["ts"], full["start"], full["count"], full["pinned"])
+    assert worst <= OUT_TOL
+    assert band == 0
+    assert layer.raas_get_status() == 0
