@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""bench.py — RaaS decode hot path on B200 (libraas), driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+A "step" is one MODEL decode step: `layers` raas_decode_step launches (one per layer handle,
+each a distinct 512 MiB KV cache at the headline config), i.e. every row of SURVEY.md §8(a)
+for every request of this rank's batch.  Requests are sharded over ranks (weak scaling: a
+fixed per-GPU batch), with no collective on the hot path.
+
+Rank 0 prints ONE JSON line.  `value` = model decode steps/s summed over GPUs (each step
+decodes `per_gpu_batch` tokens per GPU); `e2e` = the same metric through
+raas_decode_step_host (pinned host q/k/v in, out back to the host, copies inside the timed
+region); `roofline` = algorithmic HBM bytes of one raas_decode_kernel launch / its average
+duration vs MEASURED_PEAKS.json; `cpu_baseline` = the fp64 CPU oracle on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode steps/s and attention HBM GB/s (% of 8 TB/s) at L=2048, 1/2/4/8 B200"
+
+# BASELINE.json configs (shapes from the public model configs)
+CONFIGS = {
+    1: dict(workload="toy_4q2kv_d64_L64", model="toy", hq=4, hkv=2, d=64, layers=1, batch=1,
+            P=32, L=64, decode=256),
+    2: dict(workload="llama31_8b_b1_L1024", model="Llama-3.1-8B attention (32q/8kv, d=128)",
+            hq=32, hkv=8, d=128, layers=32, batch=1, P=512, L=1024, decode=8192, split_pages=2),
+    3: dict(workload="llama31_8b_b64_L2048", model="Llama-3.1-8B attention (32q/8kv, d=128)",
+            hq=32, hkv=8, d=128, layers=32, batch=64, P=256, L=2048, decode=16384),
+    4: dict(workload="r1_distill_qwen7b_b32pergpu_L4096",
+            model="DeepSeek-R1-Distill-Qwen-7B attention (28q/4kv, d=128)", hq=28, hkv=4, d=128,
+            layers=28, batch=32, P=128, L=4096, decode=32768),
+    5: dict(workload="llama31_8b_b64_budget_sweep", model="Llama-3.1-8B attention (32q/8kv, d=128)",
+            hq=32, hkv=8, d=128, layers=4, batch=64, P=128, L=2048, decode=32768),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, dev_index, period=0.02):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self._stop = period, threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            uuid_env = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = dev_index
+            if uuid_env:
+                vis = [x.strip() for x in uuid_env.split(",")]
+                if dev_index < len(vis) and vis[dev_index].isdigit():
+                    idx = int(vis[dev_index])
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            log("clock sampler unavailable:", e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------- helpers
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload):
+    """dram read+write bytes per launch of the dominant kernel, from the committed ncu
+    summary (profiles/ncu_traffic.json, written from an `ncu --set full` capture)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+def cpu_count_info():
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return n, model
+
+
+def oracle_sample(cfg, seconds=12.0, max_steps=64, seed=4242):
+    """Time the fp64 CPU oracle (as it stands) on a bounded sample of the workload: one layer,
+    `threads` units of the config from a full-cache state, steady-state decode steps until
+    `seconds` elapse.  Returns unit-steps/s and a description."""
+    import numpy as np
+
+    import oracle
+    from paper_2502_11147_b200.synth import bf16_bits, random_steady_state
+
+    threads, cpu_model = cpu_count_info()
+    threads = oracle.set_threads(threads)
+    g = cfg["hq"] // cfg["hkv"]
+    C, Pp = cfg["L"] // 16, -(-cfg["P"] // 16)
+    n_units = max(cfg["hkv"], (threads // cfg["hkv"]) * cfg["hkv"])
+    nb = n_units // cfg["hkv"]
+    d = cfg["d"]
+    t_now = Pp * 16 + 4 * 16 * (C - Pp) + 1
+    meta = random_steady_state(seed, n_units, C, Pp, t_now)
+    rng = np.random.Generator(np.random.Philox(seed + 1))
+    ks = bf16_bits(rng.standard_normal((n_units, C, 16, d), np.float32))
+    vs = bf16_bits(rng.standard_normal((n_units, C, 16, d), np.float32))
+    orc = oracle.Oracle(L=cfg["L"], alpha=1e-4, page=16, n_q_heads=nb * 0 + cfg["hq"],
+                        n_kv_heads=cfg["hkv"], head_dim=d, batch=nb)
+    orc.set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"], ks, vs)
+    steps = 0
+    t0 = time.perf_counter()
+    while steps < max_steps:
+        q = bf16_bits(2.5 * rng.standard_normal((nb, cfg["hq"], d), np.float32))
+        kn = bf16_bits(rng.standard_normal((nb, cfg["hkv"], d), np.float32))
+        vn = bf16_bits(rng.standard_normal((nb, cfg["hkv"], d), np.float32))
+        orc.decode_step(q, kn, vn)
+        steps += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    orc.close()
+    unit_steps_per_s = steps * n_units / dt
+    desc = (f"{steps} steady-state decode steps of {n_units} units ({nb} requests x "
+            f"{cfg['hkv']} kv-heads, g={g}, L={cfg['L']}, d={d}) of one layer from a full-cache "
+            f"state, {dt:.1f} s on {threads} threads ({cpu_model}); extrapolated linearly to "
+            f"{cfg['batch']} requests x {cfg['layers']} layers per step")
+    return unit_steps_per_s, threads, desc
+
+
+# ----------------------------------------------------------------------------------- main arm
+def run_ours(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2502_11147_b200 import build as build_mod
+    from paper_2502_11147_b200.raas import RaasLayer
+
+    if rank == 0 or not os.path.exists(build_mod.LIB):
+        build_mod.build()
+    if world > 1:
+        torch.distributed.barrier()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, hq, hkv, d, L, P, nl = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["d"], cfg["L"], cfg["P"], cfg["layers"]
+    g = hq // hkv
+    C = L // 16
+    Pp = -(-P // 16)
+    units = B * hkv
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 * args.config + rank)
+    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=cfg.get("split_pages", 0))
+              for _ in range(nl)]
+    info = layers[0].raas_launch_info()
+    for ly in layers:
+        k = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
+        v = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
+        ly.raas_prefill(k, v, P)
+        del k, v
+    R = 8  # ring of distinct per-step inputs
+    qs = [torch.randn((B, hq, d), device=dev, generator=gen).mul_(2.5).bfloat16() for _ in range(R)]
+    ks = [torch.randn((B, hkv, d), device=dev, generator=gen).bfloat16() for _ in range(R)]
+    vs = [torch.randn((B, hkv, d), device=dev, generator=gen).bfloat16() for _ in range(R)]
+    outs = [torch.empty((B, hq, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)]
+    stream = torch.cuda.Stream(device=dev)
+
+    # one CUDA graph per ring slot, each = one model step (nl decode launches)
+    graphs = []
+    torch.cuda.synchronize()
+    # steady state before capture: fill the decode pages once, then a further page cycle
+    fill_steps = (C - Pp) * 16 + 256 if args.fill < 0 else args.fill
+    fill_steps = min(fill_steps, cfg["decode"])
+    with torch.cuda.stream(stream):
+        for s in range(R):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=stream):
+                for li, ly in enumerate(layers):
+                    ly.raas_decode_step(qs[s], ks[s], vs[s], outs[li], stream=stream)
+            graphs.append(gr)
+    # capturing does not execute; fill now (real steps)
+    t_fill = time.perf_counter()
+    for i in range(fill_steps):
+        graphs[i % R].replay()
+    torch.cuda.synchronize()
+    t_fill = time.perf_counter() - t_fill
+    step0 = fill_steps
+    c0 = [ly.raas_get_counters() for ly in layers]
+    st0 = layers[0].raas_get_state()
+    log(f"[rank {rank}] filled {fill_steps} model steps in {t_fill:.1f}s; used pages/unit="
+        f"{(st0['count'] > 0).sum(1).mean():.1f}/{C}; launch {info}")
+
+    # warmup
+    for i in range(args.warmup):
+        graphs[(step0 + i) % R].replay()
+    step0 += args.warmup
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            graphs[(step0 + i) % R].replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    ms = ev0.elapsed_time(ev1)
+    step0 += args.steps
+    t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    ms_per_step = ms_max / args.steps
+    c1 = [ly.raas_get_counters() for ly in layers]
+    stamps = sum(b["stamps"] - a["stamps"] for a, b in zip(c0, c1))
+    decisions = sum(b["decisions"] - a["decisions"] for a, b in zip(c0, c1))
+    evictions = sum(b["evictions"] - a["evictions"] for a, b in zip(c0, c1))
+    unit_steps = sum(b["unit_steps"] - a["unit_steps"] for a, b in zip(c0, c1))
+    status = max(ly.raas_get_status() for ly in layers)
+
+    # algorithmic bytes per launch: K+V of resident tokens (steady state: the
+    # write page holds 1..16 tokens, the others are full -> mean occupancy L-7.5 over a page
+    # cycle; exact from the state at the timed steps), new K/V write, q read + out write,
+    # page metadata (ts/start/count) ~12 B per page.
+    st1 = layers[0].raas_get_state()
+    occ_now = st1["count"].sum(1).mean()
+    if (st0["count"] > 0).sum(1).min() == C:
+        occ_mean = L - 7.5
+    else:
+        occ_mean = float(occ_now)
+    bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * C)
+    launch_s = ms_per_step / 1e3 / nl
+    achieved = bytes_launch / launch_s / 1e9
+    peak, peak_src = measured_peaks()
+    model_steps_per_s = args.steps / (ms_max / 1e3)
+    value = model_steps_per_s * world
+
+    # ---------------- e2e: through raas_decode_step_host with pinned host buffers -------
+    e2e = None
+    if not args.no_e2e:
+        hq_ = [torch.empty((B, hq, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
+        hk_ = [torch.empty((B, hkv, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
+        hv_ = [torch.empty((B, hkv, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
+        ho_ = [torch.empty((B, hq, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
+        for li in range(nl):
+            hq_[li].copy_(qs[li % R].cpu())
+            hk_[li].copy_(ks[li % R].cpu())
+            hv_[li].copy_(vs[li % R].cpu())
+        e_steps = max(4, min(args.steps, 64))
+
+        def e2e_step():
+            for li, ly in enumerate(layers):
+                ly.raas_decode_step_host(hq_[li], hk_[li], hv_[li], ho_[li], stream=stream)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        e1.record(stream)
+        stream.synchronize()
+        wall = time.perf_counter() - w0
+        e_ms = max(e0.elapsed_time(e1), wall * 1e3)
+        te = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": e_steps / (float(te.item()) / 1e3) * world,
+               "unit": "decode steps/s", "steps": e_steps,
+               "h2d_bytes_per_step": nl * (B * hq * d + 2 * B * hkv * d) * 2,
+               "d2h_bytes_per_step": nl * B * hq * d * 2,
+               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out), one stream"}
+
+    if rank != 0:
+        return None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
+        cpu = {"value": ups / (units * nl), "unit": "decode steps/s", "cores": threads,
+               "kind": "oracle", "sample": desc, "unit_steps_per_s": ups}
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": f"decode steps/s (model steps: {B} requests x {nl} layers per GPU per step, summed over GPUs)",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)",
+        "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
+                   "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
+                   "page": 16, "alpha": args.alpha, "parallelism": f"request-sharded x{world}, no collective",
+                   "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
+                         "> 126 MB L2 (no flush needed)",
+                   "steady_state": f"{fill_steps} decode steps before warmup (all pages used, evicting)"},
+        "tokens_per_s": value * B,
+        "layer_steps_per_s": value * nl,
+        "hbm_gbs": achieved,
+        "pct_of_8tbs": achieved / 8000.0 * 100.0,
+        "pct_of_measured_copy": achieved / peak * 100.0,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(cfg["workload"]),
+                     "kernel": "raas_decode_kernel<128,4,3>" if d == 128 else "raas_decode_kernel<64,4,3>",
+                     "algorithmic_bytes_per_launch": bytes_launch,
+                     "avg_launch_us": launch_s * 1e6, "peak_source": peak_src,
+                     "timing": "CUDA events on the launch stream around K graph replays of "
+                               f"{nl} launches; avg launch = step / {nl}"},
+        "e2e": e2e,
+        "gpu_launches": args.steps * nl,
+        "launch": info,
+        "stamp_rate": stamps / max(decisions, 1),
+        "evictions_per_step": evictions / max(unit_steps, 1) * units,
+        "device_status": status,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    return out
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle (as it stands) on a bounded sample, same metric."""
+    if rank != 0:
+        return None
+    units = cfg["batch"] * cfg["hkv"]
+    ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
+    v = ups / (units * cfg["layers"])
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": "decode steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "per_gpu_batch": cfg["batch"], "L": cfg["L"],
+                   "layers": cfg["layers"]},
+        "cpu_baseline": {"value": v, "unit": "decode steps/s", "cores": threads, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": v, "unit": "decode steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--alpha", type=float, default=1e-4)
+    ap.add_argument("--L", type=int, default=0, help="override the budget (config 5 sweep)")
+    ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch")
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count")
+    ap.add_argument("--fill", type=int, default=-1, help="decode steps before warmup (-1: auto)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.L:
+        cfg["L"] = args.L
+        cfg["workload"] += f"_L{args.L}"
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.layers:
+        cfg["layers"] = args.layers
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, cfg, rank, world)
+    else:
+        import torch
+
+        if world > 1:
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        out = run_ours(args, cfg, rank, world, local_rank)
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

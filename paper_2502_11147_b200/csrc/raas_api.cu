@@ -78,7 +78,7 @@ int derive(const raas_config* c, Derived* d) {
   const int min_sp = (d->C + raas::MAX_SPLITS - 1) / raas::MAX_SPLITS;
   if (sp < min_sp) sp = min_sp;
   if (sp > d->C) sp = d->C;
-  if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "L too large (more than 32*32 pages)");
+  if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "L too large (more than 32*128 pages)");
   d->split_pages = sp;
   d->nsplit = (d->C + sp - 1) / sp;
   return RAAS_OK;

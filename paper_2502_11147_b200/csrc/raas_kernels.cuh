@@ -22,7 +22,7 @@ namespace raas {
 
 constexpr int PAGE = 16;
 constexpr int MAX_GROUP = 8;
-constexpr int MAX_SPLITS = 32;
+constexpr int MAX_SPLITS = 128;   // splits per unit (combine: 4 per lane)
 
 struct DecodeParams {
   const __nv_bfloat16* q;      // [units*g][D]
@@ -331,27 +331,44 @@ __global__ void __launch_bounds__(NW * 32)
         for (int h = 0; h < MAX_GROUP; ++h) {
           lse[h] = 0.f;
           if (h < g) {
-            const float2 ml = lane < nse
-                                  ? __ldcg(p.part_ml + (unit * p.nsplit + lane) * g + h)
-                                  : make_float2(-INFINITY, 0.f);
-            const float M = warp_max(ml.x);
-            const float w = lane < nse ? fast_exp2(ml.x - M) : 0.f;
-            const float Lh = warp_sum(ml.y * w);
+            constexpr int SPL = MAX_SPLITS / 32;  // splits per lane
+            float ms[SPL], w[SPL], lsum = 0.f, M = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+              const int sp = lane + 32 * k;
+              const float2 ml = sp < nse ? __ldcg(p.part_ml + (unit * p.nsplit + sp) * g + h)
+                                         : make_float2(-INFINITY, 0.f);
+              ms[k] = ml.x;
+              w[k] = ml.y;  // holds l until the weights are known
+              M = fmaxf(M, ml.x);
+            }
+            M = warp_max(M);
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+              const float l_k = w[k];
+              w[k] = lane + 32 * k < nse ? fast_exp2(ms[k] - M) : 0.f;
+              lsum += l_k * w[k];
+            }
+            const float Lh = warp_sum(lsum);
             lse[h] = M + log2f(Lh);  // log2-domain LSE of head h
             const float inv = 1.f / Lh;
             float o[DPL];
 #pragma unroll
             for (int i = 0; i < DPL; ++i) o[i] = 0.f;
-            for (int sp = 0; sp < nse; ++sp) {
-              const float ws = __shfl_sync(0xffffffffu, w, sp);
-              const float* src =
-                  p.part_acc + (size_t)((unit * p.nsplit + sp) * g + h) * D + lane * DPL;
-              if constexpr (DPL == 4) {
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-                o[0] += ws * v.x; o[1] += ws * v.y; o[2] += ws * v.z; o[3] += ws * v.w;
-              } else {
-                const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
-                o[0] += ws * v.x; o[1] += ws * v.y;
+#pragma unroll
+            for (int k = 0; k < SPL; ++k) {
+              for (int j = 0; j < 32 && 32 * k + j < nse; ++j) {
+                const int sp = 32 * k + j;
+                const float ws = __shfl_sync(0xffffffffu, w[k], j);
+                const float* src =
+                    p.part_acc + (size_t)((unit * p.nsplit + sp) * g + h) * D + lane * DPL;
+                if constexpr (DPL == 4) {
+                  const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+                  o[0] += ws * v.x; o[1] += ws * v.y; o[2] += ws * v.z; o[3] += ws * v.w;
+                } else {
+                  const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
+                  o[0] += ws * v.x; o[1] += ws * v.y;
+                }
               }
             }
             __nv_bfloat16* dst = p.out + (size_t)(unit * g + h) * D + lane * DPL;
