@@ -152,7 +152,7 @@ def cpu_count_info():
     return n, model
 
 
-def oracle_sample(cfg, seconds=12.0, max_steps=64, seed=4242):
+def oracle_sample(cfg, seconds=12.0, max_steps=100000, seed=4242):
     """Time the fp64 CPU oracle (as it stands) on a bounded sample of the workload: one layer,
     `threads` units of the config from a full-cache state, steady-state decode steps until
     `seconds` elapse.  Returns unit-steps/s and a description."""
@@ -247,8 +247,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             graphs.append(gr)
     # capturing does not execute; fill now (real steps)
     t_fill = time.perf_counter()
-    for i in range(fill_steps):
-        graphs[i % R].replay()
+    with torch.cuda.stream(stream):  # CUDAGraph.replay() launches on the current stream
+        for i in range(fill_steps):
+            graphs[i % R].replay()
     torch.cuda.synchronize()
     t_fill = time.perf_counter() - t_fill
     step0 = fill_steps
@@ -258,8 +259,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         f"{(st0['count'] > 0).sum(1).mean():.1f}/{C}; launch {info}")
 
     # warmup
-    for i in range(args.warmup):
-        graphs[(step0 + i) % R].replay()
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            graphs[(step0 + i) % R].replay()
     step0 += args.warmup
     torch.cuda.synchronize()
     if world > 1:
@@ -269,10 +271,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
-        ev0.record(stream)
-        for i in range(args.steps):
-            graphs[(step0 + i) % R].replay()
-        ev1.record(stream)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for i in range(args.steps):
+                graphs[(step0 + i) % R].replay()
+            ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -304,6 +307,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     launch_s = ms_per_step / 1e3 / nl
     achieved = bytes_launch / launch_s / 1e9
     peak, peak_src = measured_peaks()
+    if achieved > 1.3 * peak:
+        raise RuntimeError(f"achieved {achieved:.0f} GB/s > 1.3x the copy peak: the timed region "
+                           "did not do the work")
     model_steps_per_s = args.steps / (ms_max / 1e3)
     value = model_steps_per_s * world
 

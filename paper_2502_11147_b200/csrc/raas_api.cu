@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/raas.h"
@@ -37,14 +38,14 @@ int fail(int code, const char* fmt, ...) {
 constexpr size_t ALIGN = 1024;
 size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
-// decode kernel shape (tuned on B200)
-constexpr int NW = 4;      // warps per CTA (each an independent worker)
-constexpr int STAGES = 3;  // pages in flight per warp
-
+// decode kernel shape (B200): one persistent CTA per SM with a TMA producer
+// warp, a merge/combine warp and NC consumer warps sharing a ring of S page stages.
+constexpr int NC = 8;   // consumer (MMA) warps per CTA
+constexpr int S = 16;   // K+V page stages in the ring (8 KiB each at head_dim 128)
 template <int D>
-constexpr int smem_bytes() {
-  return 1024 + NW * STAGES * (2 * raas::PAGE * D * 2) + NW * STAGES * (8 + 32);
-}
+using Lay = raas::DecodeLayout<D, NC, S>;
+template <int D>
+constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
   size_t kstore, vstore, ts, start, cnt, npin, plan, counter, pmax, part_acc, part_ml, status,
@@ -73,12 +74,13 @@ int derive(const raas_config* c, Derived* d) {
   d->units = c->batch * c->n_kv_heads;
   if ((long long)d->units * d->C * raas::PAGE >= (1LL << 31))
     return fail(RAAS_E_UNSUPPORTED, "units * L too large for 32-bit TMA row coordinates");
-  int sp = c->split_pages > 0 ? c->split_pages : 8;
+  // auto: a quarter of the budget per split, 4..32 pages (depends on L only, never on batch)
+  int sp = c->split_pages > 0 ? c->split_pages : std::max(4, std::min(32, d->C / 4));
   if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "split_pages must be <= 32");
   const int min_sp = (d->C + raas::MAX_SPLITS - 1) / raas::MAX_SPLITS;
   if (sp < min_sp) sp = min_sp;
   if (sp > d->C) sp = d->C;
-  if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "L too large (more than 32*128 pages)");
+  if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "L too large (more than 32*%d pages)", raas::MAX_SPLITS);
   d->split_pages = sp;
   d->nsplit = (d->C + sp - 1) / sp;
   return RAAS_OK;
@@ -187,7 +189,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
 
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(h->grid);
-  lc.blockDim = dim3(NW * 32);
+  lc.blockDim = dim3(Lay<D>::THREADS);
   lc.dynamicSmemBytes = h->smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
@@ -195,20 +197,19 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  RAAS_CUDA(cudaLaunchKernelEx(&lc, raas::raas_decode_kernel<D, NW, STAGES>, p, h->tmK, h->tmV));
+  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D>(), p, h->tmK, h->tmV));
   return RAAS_OK;
 }
 
 template <int D>
 int setup_kernel(raas_handle* h) {
-  auto k = raas::raas_decode_kernel<D, NW, STAGES>;
-  h->smem = smem_bytes<D>();
+  auto k = decode_kernel<D>();
+  h->smem = Lay<D>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
-  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NW * 32, h->smem));
+  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
-  const long long tiles = (long long)h->d.units * h->d.nsplit;
-  const long long need = (tiles + NW - 1) / NW;
+  const long long need = (long long)h->d.units * h->d.nsplit;  // one tile per CTA at most
   const long long cap = (long long)h->num_sms * per_sm;
   h->grid = (int)(need < cap ? need : cap);
   return RAAS_OK;
@@ -480,7 +481,7 @@ int raas_get_counters(raas_handle* h, uint64_t counters[4], void* stream) {
 int raas_launch_info(const raas_handle* h, int32_t info[5]) {
   if (!h || !info) return fail(RAAS_E_INVALID, "null argument");
   info[0] = h->grid;
-  info[1] = NW * 32;
+  info[1] = h->cfg.head_dim == 128 ? Lay<128>::THREADS : Lay<64>::THREADS;
   info[2] = h->smem;
   info[3] = h->d.split_pages;
   info[4] = h->d.nsplit;

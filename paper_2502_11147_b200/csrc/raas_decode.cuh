@@ -1,0 +1,486 @@
+// raas_decode.cuh — the fused RaaS decode-step kernel (sm_100a), warp-specialized.
+//
+// One launch = one decode step of one layer (handle) for every unit (request, kv-head):
+//   a1 slot selection (from the plan computed at the end of the previous step)
+//   a2 in-place write of k_new / v_new into the slot (smem tile + HBM store)
+//   a3 split-K flash-decode over the resident pages        (consumer warps, mma.sync bf16)
+//   a4 page-max logits M_{h,p}                             (consumer warps)
+//   a5 LSE combine across splits, bf16 output              (combine warp, last split of a unit)
+//   a6 stamp: ts[p] = t iff max_h M_{h,p} - LSE_h > log2(alpha)   (combine warp)
+//   a7 next victim = argmin_{unpinned} (ts, start_pos); next plan  (combine warp)
+// PAPER.md §3.3 :143-151, App. B :358-398; readings D1-D20 in DESIGN.md.
+//
+// CTA (persistent, one per SM; tiles (unit, split) of SP pages, static order blockIdx + k*grid):
+//   warp 0         TMA producer: per page one 2-D TMA of the K page and one of the V page
+//                  (16 x D bf16, 128B swizzle) into a ring of S stages; per tile a bulk copy of
+//                  the unit's q rows; prefetches the next tile's plan / page counts.
+//   warp 1         merge + combine: merges the consumers' per-tile softmax states (smem),
+//                  publishes the tile's split-K partial, and for a unit's last split runs
+//                  a5-a7.  Never consumes ring stages, so its latency does not stall HBM.
+//   warps 2..NC+1  consumers: ring position j goes to consumer j % NC; per page
+//                  S^T = K_page Q^T and O^T += V_page^T P^T on mma.sync m16n8k16 (16 tokens = M,
+//                  the <= 8 q-heads of the GQA group = N), online softmax in fp32 registers.
+#pragma once
+
+namespace raas {
+
+constexpr int FLAG_FIRST = 1;  // first page of this tile for the consuming warp
+constexpr int FLAG_LAST = 2;   // last page of this tile for the consuming warp
+constexpr int FLAG_END = 4;    // no more work
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(n) : "memory");
+}
+// 1-D bulk copy global -> shared (size multiple of 16), completion counted on `bar`.
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+template <int D, int NC, int S>
+struct DecodeLayout {
+  static constexpr int KS = D / 16;
+  static constexpr int TILE = PAGE * D * 2;  // one K (or V) page
+  static constexpr int STAGE = 2 * TILE;
+  static constexpr int QBUF = MAX_GROUP * D * 2;
+  static constexpr int FRAG = KS * 4 + 4;  // floats per lane in a consumer's deposit
+  static constexpr int DEPOSIT = FRAG * 32 * 4;
+  static constexpr int OFF_RING = 0;
+  static constexpr int OFF_Q = OFF_RING + S * STAGE;
+  static constexpr int OFF_MERGE = OFF_Q + 2 * QBUF;
+  static constexpr int OFF_SCR = OFF_MERGE + 2 * NC * DEPOSIT;            // combine scratch
+  static constexpr int SCR = MAX_SPLITS * MAX_GROUP * 8 + 2 * MAX_GROUP * 4;
+  static constexpr int OFF_SINFO = OFF_SCR + SCR;                          // int4[2] per stage
+  static constexpr int OFF_TINFO = OFF_SINFO + S * 32;                     // int4[2] per parity
+  static constexpr int OFF_BAR = OFF_TINFO + 2 * 32;
+  static constexpr int NBAR = 2 * S + 6;  // full[S], empty[S], qfull[2], mfull[2], tfree[2]
+  static constexpr int BYTES = OFF_BAR + NBAR * 8;
+  static constexpr int SMEM = BYTES + 1024;  // + alignment slack
+  static constexpr int THREADS = (NC + 2) * 32;
+};
+
+// ---------------------------------------------------------------------------------------------
+// a5-a7 for one unit, by one warp, after all its splits have published their partials.
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, uint32_t scr,
+                                             int lane) {
+  const int C = p.C, g = p.g, SP = p.split_pages;
+  const int4 pl = __ldcg(p.plan + unit);
+  const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
+  const int used_eff = pl.z, t = pl.w;
+  const int npin = __ldg(p.npin + unit);
+  const int nse = (used_eff + SP - 1) / SP;
+  const int NE = nse * g;
+  const uint32_t scr_ml = scr;                                  // float2[nse][g]
+  const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
+  const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
+  const float2* ml_g = p.part_ml + (size_t)unit * p.nsplit * g;
+#pragma unroll 4
+  for (int i = lane; i < NE; i += 32) {
+    const float2 ml = __ldcg(ml_g + i);
+    sts_f32(scr_ml + 8 * i, ml.x);
+    sts_f32(scr_ml + 8 * i + 4, ml.y);
+  }
+  __syncwarp();
+  if (lane < g) {  // a5: LSE_h = M + log2 sum_s 2^(m_s - M) l_s  (log2 domain)
+    float M = -INFINITY;
+    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_ml + 8 * (s * g + lane)));
+    float L = 0.f;
+    for (int s = 0; s < nse; ++s) {
+      const uint32_t a = scr_ml + 8 * (s * g + lane);
+      const float w = fast_exp2(lds_f32(a) - M);
+      L += w * lds_f32(a + 4);
+      sts_f32(a, w);  // keep the split weight in place of m_s
+    }
+    sts_f32(scr_lse + 4 * lane, M + log2f(L));
+    sts_f32(scr_inv + 4 * lane, 1.f / L);
+  }
+  __syncwarp();
+  // out[h][d] = sum_s w_s acc_s[h][d] / L_h, 4 dims per chunk
+  constexpr int CPH = D / 4;  // chunks per head
+  const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
+  for (int c = lane; c < g * CPH; c += 32) {
+    const int h = c / CPH, d4 = c - h * CPH;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s = 0; s < nse; ++s) {
+      const float w = lds_f32(scr_ml + 8 * (s * g + h));
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)s * g + h) * D) + d4);
+      o.x += w * v.x; o.y += w * v.y; o.z += w * v.z; o.w += w * v.w;
+    }
+    const float inv = lds_f32(scr_inv + 4 * h);
+    uint2 pk = make_uint2(pack_bf16x2(o.x * inv, o.y * inv), pack_bf16x2(o.z * inv, o.w * inv));
+    *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) = pk;
+  }
+  // a6: stamp; a2 metadata of the write slot; a7 candidates
+  float lse[MAX_GROUP];
+#pragma unroll
+  for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
+  Cand best{~0ull, -1};
+  int n_stamp = 0, n_dec = 0;
+#pragma unroll 2
+  for (int pg = lane; pg < used_eff; pg += 32) {
+    const size_t ix = (size_t)unit * C + pg;
+    int ts_p = __ldcg(p.ts + ix), st_p = __ldcg(p.start + ix);
+    const bool is_slot = pg == slot;
+    if (is_slot) {
+      if (off == 0) { st_p = t; p.start[ix] = t; }
+      p.cnt[ix] = off + 1;
+    }
+    if (pg >= npin) {
+      float x = -INFINITY;
+      const float* pm = p.pmax + ix * g;
+#pragma unroll
+      for (int h = 0; h < MAX_GROUP; ++h)
+        if (h < g) x = fmaxf(x, __ldcg(pm + h) - lse[h]);
+      const bool stamp = x > p.log2_alpha;  // strict (D3)
+      ++n_dec;
+      n_stamp += stamp ? 1 : 0;
+      if (stamp || is_slot) { ts_p = t; p.ts[ix] = t; }  // stamp, or write refresh (D8)
+      cand_update(best, cand_key(ts_p, st_p), pg);
+    }
+  }
+  const int victim = warp_argmin_page(best);
+  n_stamp = warp_sum_i(n_stamp);
+  n_dec = warp_sum_i(n_dec);
+  if (lane == 0) {
+    p.plan[unit] = next_plan(slot, off + 1, used_eff, C, t, victim, p.status);
+    p.counter[unit] = 0;
+    atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
+    atomicAdd(p.stats + 1, (unsigned long long)n_dec);
+    if (evicting) atomicAdd(p.stats + 2, 1ull);
+    atomicAdd(p.stats + 3, 1ull);
+  }
+}
+
+template <int D, int NC, int S>
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
+    raas_decode_kernel(const __grid_constant__ DecodeParams p,
+                       const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV) {
+  static_assert(D == 64 || D == 128, "head_dim");
+  using Lay = DecodeLayout<D, NC, S>;
+  constexpr int KS = Lay::KS, HALVES = D / 64, TILE = Lay::TILE, STAGE = Lay::STAGE;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // 128B-swizzle atoms need 1024B alignment
+  const uint32_t ring = base + Lay::OFF_RING, qbuf = base + Lay::OFF_Q;
+  const uint32_t merge = base + Lay::OFF_MERGE, scr = base + Lay::OFF_SCR;
+  int4* sinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_SINFO);
+  int4* tinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_TINFO);
+  const uint32_t bar = base + Lay::OFF_BAR;
+  auto full = [&](int s) { return bar + 8 * s; };
+  auto empty = [&](int s) { return bar + 8 * (S + s); };
+  auto qfull = [&](int par) { return bar + 8 * (2 * S + par); };
+  auto mfull = [&](int par) { return bar + 8 * (2 * S + 2 + par); };
+  auto tfree = [&](int par) { return bar + 8 * (2 * S + 4 + par); };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int par = 0; par < 2; ++par) {
+      mbar_init(qfull(par), 1);
+      mbar_init(mfull(par), NC);
+      mbar_init(tfree(par), 1);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  __syncthreads();
+  pdl_wait();  // everything above overlapped the previous kernel; state reads start here
+  pdl_launch_dependents();
+
+  const int C = p.C, SP = p.split_pages, g = p.g;
+  const int n_tiles = p.units * p.nsplit;
+
+  if (warp == 0) {
+    // =============================== TMA producer ===============================
+    const uint64_t pol = l2_evict_first_policy();
+    int4 nplan = make_int4(0, 0, 0, 0);
+    int ncnt = 0;
+    auto fetch = [&](int tl) {
+      if (tl < n_tiles) {
+        const int u = tl / p.nsplit, q0 = (tl - u * p.nsplit) * SP;
+        nplan = p.plan[u];
+        ncnt = (lane < SP && q0 + lane < C) ? p.cnt[(size_t)u * C + q0 + lane] : 0;
+      }
+    };
+    fetch(blockIdx.x);
+    uint32_t j = 0;
+    int k = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int unit = tile / p.nsplit, split = tile - unit * p.nsplit;
+      const int4 pl = nplan;
+      const int cntv = ncnt;
+      fetch(tile + gridDim.x);  // next tile's metadata, in flight while this tile is issued
+      const int used_eff = pl.z, p0 = split * SP;
+      const int n = min(p0 + SP, used_eff) - p0;
+      if (n <= 0) continue;  // pages not yet allocated (fill phase)
+      const int slot = pl.x, off = pl.y & 0xffff;
+      const int par = k & 1;
+      mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1);  // tile k-2 merged: its q/info/deposits free
+      if (lane == 0) {
+        tinfo[2 * par] = make_int4(unit, split, (used_eff + SP - 1) / SP, n);
+        tinfo[2 * par + 1] = make_int4((int)j, 0, 0, 0);
+        mbar_arrive_expect_tx(qfull(par), g * D * 2);
+        bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
+        if (n < NC) mbar_arrive_cnt(mfull(par), NC - n);  // warps with no page in this tile
+      }
+      for (int i = 0; i < n; ++i, ++j) {
+        const int s = (int)(j % S);
+        const int page = p0 + i;
+        const int c = __shfl_sync(0xffffffffu, cntv, i);
+        mbar_wait(empty(s), ((j / S) & 1) ^ 1);
+        if (lane == 0) {
+          const bool is_slot = page == slot;
+          sinfo[2 * s] = make_int4(unit, page, is_slot ? off + 1 : c, is_slot ? off : -1);
+          sinfo[2 * s + 1] =
+              make_int4(k, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
+          mbar_arrive_expect_tx(full(s), STAGE);
+          const int32_t y = (unit * C + page) * PAGE;
+          const uint32_t dk = ring + s * STAGE, dv = dk + TILE;
+#pragma unroll
+          for (int hf = 0; hf < HALVES; ++hf) {
+            tma_load_2d(dk + hf * 2048, &tmK, hf * 64, y, full(s), pol);
+            tma_load_2d(dv + hf * 2048, &tmV, hf * 64, y, full(s), pol);
+          }
+        }
+        __syncwarp();
+      }
+      ++k;
+    }
+    for (int e = 0; e < NC; ++e, ++j) {  // one END sentinel per consumer
+      const int s = (int)(j % S);
+      mbar_wait(empty(s), ((j / S) & 1) ^ 1);
+      if (lane == 0) {
+        sinfo[2 * s + 1] = make_int4(0, FLAG_END, 0, 0);
+        mbar_arrive(full(s));
+      }
+      __syncwarp();
+    }
+    const int par = k & 1;  // END for the merge warp
+    mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1);
+    if (lane == 0) {
+      tinfo[2 * par + 1] = make_int4(0, FLAG_END, 0, 0);
+      mbar_arrive_cnt(mfull(par), NC);
+    }
+  } else if (warp == 1) {
+    // ====================== merge (per tile) + combine (per unit) ======================
+    const int r = lane >> 2, qd = lane & 3;
+    for (int k = 0;; ++k) {
+      const int par = k & 1;
+      mbar_wait(mfull(par), (k >> 1) & 1);
+      const int4 t0 = tinfo[2 * par], t1 = tinfo[2 * par + 1];
+      if (t1.y & FLAG_END) break;
+      const int unit = t0.x, split = t0.y, nse = t0.z, n = t0.w, J = t1.x;
+      const int nw = min(n, NC);
+      float acc[KS * 4];
+#pragma unroll
+      for (int i = 0; i < KS * 4; ++i) acc[i] = 0.f;
+      float M0 = -INFINITY, M1 = -INFINITY, L0 = 0.f, L1 = 0.f;
+      for (int i = 0; i < nw; ++i) {
+        const uint32_t dep = merge + (par * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
+        M0 = fmaxf(M0, lds_f32(dep + 128 * (KS * 4 + 0)));
+        M1 = fmaxf(M1, lds_f32(dep + 128 * (KS * 4 + 1)));
+      }
+      for (int i = 0; i < nw; ++i) {
+        const uint32_t dep = merge + (par * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
+        const float s0 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 0)) - M0);
+        const float s1 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 1)) - M1);
+        L0 += s0 * lds_f32(dep + 128 * (KS * 4 + 2));
+        L1 += s1 * lds_f32(dep + 128 * (KS * 4 + 3));
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          acc[4 * mt + 0] += s0 * lds_f32(dep + 128 * (4 * mt + 0));
+          acc[4 * mt + 1] += s1 * lds_f32(dep + 128 * (4 * mt + 1));
+          acc[4 * mt + 2] += s0 * lds_f32(dep + 128 * (4 * mt + 2));
+          acc[4 * mt + 3] += s1 * lds_f32(dep + 128 * (4 * mt + 3));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tfree(par));  // deposits / q / info of tile k consumed
+      // publish the tile's split-K partial (m, l, acc) in the C-fragment layout
+      const int pbase = (unit * p.nsplit + split) * g;
+      if (lane < 4) {
+        if (2 * qd < g) p.part_ml[pbase + 2 * qd] = make_float2(M0, L0);
+        if (2 * qd + 1 < g) p.part_ml[pbase + 2 * qd + 1] = make_float2(M1, L1);
+      }
+      float* pa0 = p.part_acc + (size_t)(pbase + 2 * qd) * D + r;
+      float* pa1 = pa0 + D;
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        if (2 * qd < g) { pa0[16 * mt] = acc[4 * mt + 0]; pa0[16 * mt + 8] = acc[4 * mt + 2]; }
+        if (2 * qd + 1 < g) { pa1[16 * mt] = acc[4 * mt + 1]; pa1[16 * mt + 8] = acc[4 * mt + 3]; }
+      }
+      __threadfence();
+      __syncwarp();
+      int old = 0;
+      if (lane == 0) old = atomicAdd(p.counter + unit, 1);
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old == nse - 1) {  // this was the unit's last split
+        __threadfence();
+        combine_unit<D>(p, unit, scr, lane);
+      }
+    }
+  } else {
+    // ================================ consumers ================================
+    const int w = warp - 2;
+    const int r = lane >> 2, qd = lane & 3;   // C-fragment row (token) / column pair (head)
+    const int mi = lane >> 3, ri = lane & 7;  // ldmatrix matrix / row supplied by this lane
+    float acc[KS][4];
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    uint32_t qb[KS][2];
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+      qb[mt][0] = qb[mt][1] = 0u;
+    }
+    for (uint32_t j = w;; j += NC) {
+      const int s = (int)(j % S);
+      mbar_wait(full(s), (j / S) & 1);
+      const int4 i0 = sinfo[2 * s], i1 = sinfo[2 * s + 1];
+      const int flags = i1.y;
+      if (flags & FLAG_END) break;
+      const int unit = i0.x, page = i0.y, cnt = i0.z, patch = i0.w, k = i1.x, par = k & 1;
+      const uint32_t kb = ring + s * STAGE, vb = kb + TILE;
+
+      if (flags & FLAG_FIRST) {  // fresh softmax state; this unit's q fragments from smem
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
+        m0 = m1 = -INFINITY;
+        l0 = l1 = 0.f;
+        mbar_wait(qfull(par), (k >> 1) & 1);
+        const uint32_t qrow = qbuf + par * Lay::QBUF + r * D * 2 + qd * 4;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          qb[ks][0] = r < g ? lds_u32(qrow + ks * 32) : 0u;       // d = 16ks + 2qd, +1
+          qb[ks][1] = r < g ? lds_u32(qrow + ks * 32 + 16) : 0u;  // d = 16ks + 8 + 2qd, +1
+        }
+      }
+
+      if (patch >= 0) {  // a2: the new token's K/V into row `patch` (smem tile + HBM store)
+        constexpr int NCH = D / 8;
+        if (lane < 2 * NCH) {
+          const bool isv = lane >= NCH;
+          const int ch = isv ? lane - NCH : lane;
+          const uint4 val = __ldg(reinterpret_cast<const uint4*>(
+                                      (isv ? p.v_new : p.k_new) + (size_t)unit * D) + ch);
+          const uint32_t sa = (isv ? vb : kb) + (ch >> 3) * 2048 + patch * 128 +
+                              (((ch & 7) ^ (patch & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa), "r"(val.x),
+                       "r"(val.y), "r"(val.z), "r"(val.w)
+                       : "memory");
+          *reinterpret_cast<uint4*>((isv ? p.vstore : p.kstore) +
+                                    ((size_t)(unit * C + page) * PAGE + patch) * D + ch * 8) = val;
+          fence_proxy_async_smem();  // before the stage is refilled by TMA
+        }
+        __syncwarp();
+      }
+
+      // ---- a3/a4: S^T = K_page Q^T (M = 16 tokens, N = 8 heads, K = D) ----
+      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+      {
+        const uint32_t krow = kb + (ri + 8 * (mi & 1)) * 128;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t a[4];
+          const int chunk = 2 * (ks & 3) + (mi >> 1);
+          ldsm_x4(krow + (ks >> 2) * 2048 + ((chunk ^ ri) << 4), a);
+          if (ks & 1) mma_bf16_16816(c1, a, qb[ks][0], qb[ks][1]);
+          else        mma_bf16_16816(c0, a, qb[ks][0], qb[ks][1]);
+        }
+      }
+      float s0 = (c0[0] + c1[0]) * p.scale_log2, s1 = (c0[1] + c1[1]) * p.scale_log2;
+      float s2 = (c0[2] + c1[2]) * p.scale_log2, s3 = (c0[3] + c1[3]) * p.scale_log2;
+      if (r >= cnt) s0 = s1 = -INFINITY;
+      if (r + 8 >= cnt) s2 = s3 = -INFINITY;
+      float pm0 = fmaxf(s0, s2), pm1 = fmaxf(s1, s3);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        pm0 = fmaxf(pm0, __shfl_xor_sync(0xffffffffu, pm0, o));
+        pm1 = fmaxf(pm1, __shfl_xor_sync(0xffffffffu, pm1, o));
+      }
+      if (lane < 4) {  // a4: page-max logit per head ("a single attention score per page", :147)
+        float* pmx = p.pmax + (size_t)(unit * C + page) * g;
+        if (2 * qd < g) pmx[2 * qd] = pm0;
+        if (2 * qd + 1 < g) pmx[2 * qd + 1] = pm1;
+      }
+      const float mn0 = fmaxf(m0, pm0), mn1 = fmaxf(m1, pm1);
+      const float cr0 = fast_exp2(m0 - mn0), cr1 = fast_exp2(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      const float p0 = fast_exp2(s0 - mn0), p1 = fast_exp2(s1 - mn1);
+      const float p2 = fast_exp2(s2 - mn0), p3 = fast_exp2(s3 - mn1);
+      l0 = l0 * cr0 + (p0 + p2);
+      l1 = l1 * cr1 + (p1 + p3);
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        acc[mt][0] *= cr0;
+        acc[mt][1] *= cr1;
+        acc[mt][2] *= cr0;
+        acc[mt][3] *= cr1;
+      }
+      // P^T as the B operand of O^T = V^T P^T: transpose the two 8x8 bf16 blocks in registers
+      const uint32_t b0 = movmatrix_t(pack_bf16x2(p0, p1));
+      const uint32_t b1 = movmatrix_t(pack_bf16x2(p2, p3));
+      {
+        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * 128;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          uint32_t a[4];
+          const int chunk = 2 * (mt & 3) + (mi & 1);
+          ldsm_x4_t(vrow + (mt >> 2) * 2048 + ((chunk ^ ri) << 4), a);
+          mma_bf16_16816(acc[mt], a, b0, b1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(s));  // stage free for the producer
+
+      if (flags & FLAG_LAST) {  // deposit this warp's softmax state for the tile merge
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+          l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        }
+        const uint32_t dep = merge + (par * NC + w) * Lay::DEPOSIT + 4 * lane;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sts_f32(dep + 128 * (4 * mt + e), acc[mt][e]);
+        sts_f32(dep + 128 * (KS * 4 + 0), m0);
+        sts_f32(dep + 128 * (KS * 4 + 1), m1);
+        sts_f32(dep + 128 * (KS * 4 + 2), l0);
+        sts_f32(dep + 128 * (KS * 4 + 3), l1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mfull(par));
+      }
+    }
+  }
+}
+
+}  // namespace raas
