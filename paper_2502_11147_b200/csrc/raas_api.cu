@@ -1,8 +1,6 @@
 // raas_api.cu — host side of libraas: config validation, arena carving, TMA descriptors,
 // launches.  The C ABI is declared (and documented, with citations) in include/raas.h.
-#include <cuda.h>
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -125,17 +123,17 @@ struct DeviceGuard {
   }
 };
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
+// Host view of the KV store is [units][C][16][D] in logical order; on the device each token row
+// keeps its 16-byte chunk c at chunk c ^ (row & 7) (see raas_kernels.cuh).  This permutes a
+// whole store between the two (the permutation is an involution).
+void swizzle_store(const uint16_t* src, uint16_t* dst, size_t pages, int D) {
+  const int nch = D / 8;
+  for (size_t pg = 0; pg < pages; ++pg)
+    for (int r = 0; r < raas::PAGE; ++r) {
+      const uint16_t* srow = src + (pg * raas::PAGE + r) * D;
+      uint16_t* drow = dst + (pg * raas::PAGE + r) * D;
+      for (int c = 0; c < nch; ++c) std::memcpy(drow + (c ^ (r & 7)) * 8, srow + c * 8, 16);
+    }
 }
 
 }  // namespace
@@ -150,7 +148,6 @@ struct raas_handle {
   int smem;
   uint8_t* arena;
   int prefilled;
-  CUtensorMap tmK, tmV;
 };
 
 namespace {
@@ -197,7 +194,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D>(), p, h->tmK, h->tmV));
+  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D>(), p));
   return RAAS_OK;
 }
 
@@ -212,22 +209,6 @@ int setup_kernel(raas_handle* h) {
   const long long need = (long long)h->d.units * h->d.nsplit;  // one tile per CTA at most
   const long long cap = (long long)h->num_sms * per_sm;
   h->grid = (int)(need < cap ? need : cap);
-  return RAAS_OK;
-}
-
-int make_tmap(raas_handle* h, CUtensorMap* m, void* base) {
-  auto enc = get_encode();
-  if (!enc) return fail(RAAS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t D = h->cfg.head_dim;
-  const cuuint64_t rows = (cuuint64_t)h->d.units * h->d.C * raas::PAGE;
-  cuuint64_t gdim[2] = {D, rows};
-  cuuint64_t gstride[1] = {D * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)raas::PAGE};
-  cuuint32_t estride[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, gdim, gstride, box, estride,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(RAAS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return RAAS_OK;
 }
 
@@ -282,8 +263,6 @@ int raas_create(const raas_config* cfg, void* arena, size_t arena_bytes, int dev
   }
   h->num_sms = sms;
   rc = cfg->head_dim == 128 ? setup_kernel<128>(h) : setup_kernel<64>(h);
-  if (!rc) rc = make_tmap(h, &h->tmK, h->arena + lay.kstore);
-  if (!rc) rc = make_tmap(h, &h->tmV, h->arena + lay.vstore);
   if (!rc) {
     e = cudaMemset(arena, 0, lay.total);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -434,10 +413,17 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.npin, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.plan, plan.data(), U * 16, cudaMemcpyHostToDevice, st));
   const size_t kvb = U * C * raas::PAGE * h->cfg.head_dim * 2;
-  if (k_store_host)
-    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kstore, k_store_host, kvb, cudaMemcpyHostToDevice, st));
-  if (v_store_host)
-    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.vstore, v_store_host, kvb, cudaMemcpyHostToDevice, st));
+  std::vector<uint16_t> ksw, vsw;
+  if (k_store_host) {
+    ksw.resize(kvb / 2);
+    swizzle_store(static_cast<const uint16_t*>(k_store_host), ksw.data(), U * C, h->cfg.head_dim);
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kstore, ksw.data(), kvb, cudaMemcpyHostToDevice, st));
+  }
+  if (v_store_host) {
+    vsw.resize(kvb / 2);
+    swizzle_store(static_cast<const uint16_t*>(v_store_host), vsw.data(), U * C, h->cfg.head_dim);
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.vstore, vsw.data(), kvb, cudaMemcpyHostToDevice, st));
+  }
   int rc = refresh(h, st);
   if (rc) return rc;
   RAAS_CUDA(cudaStreamSynchronize(st));
@@ -449,12 +435,17 @@ int raas_get_kv(raas_handle* h, void* k_store_host, void* v_store_host, void* st
   if (!h) return fail(RAAS_E_INVALID, "null handle");
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t kvb = (size_t)h->d.units * h->d.C * raas::PAGE * h->cfg.head_dim * 2;
-  if (k_store_host)
-    RAAS_CUDA(cudaMemcpyAsync(k_store_host, h->arena + h->lay.kstore, kvb, cudaMemcpyDeviceToHost, st));
-  if (v_store_host)
-    RAAS_CUDA(cudaMemcpyAsync(v_store_host, h->arena + h->lay.vstore, kvb, cudaMemcpyDeviceToHost, st));
-  RAAS_CUDA(cudaStreamSynchronize(st));
+  const size_t pages = (size_t)h->d.units * h->d.C;
+  const size_t kvb = pages * raas::PAGE * h->cfg.head_dim * 2;
+  std::vector<uint16_t> tmp(kvb / 2);
+  void* outs[2] = {k_store_host, v_store_host};
+  const size_t offs[2] = {h->lay.kstore, h->lay.vstore};
+  for (int i = 0; i < 2; ++i) {
+    if (!outs[i]) continue;
+    RAAS_CUDA(cudaMemcpyAsync(tmp.data(), h->arena + offs[i], kvb, cudaMemcpyDeviceToHost, st));
+    RAAS_CUDA(cudaStreamSynchronize(st));
+    swizzle_store(tmp.data(), static_cast<uint16_t*>(outs[i]), pages, h->cfg.head_dim);
+  }
   return RAAS_OK;
 }
 

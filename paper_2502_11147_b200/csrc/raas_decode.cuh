@@ -11,9 +11,10 @@
 // PAPER.md §3.3 :143-151, App. B :358-398; readings D1-D20 in DESIGN.md.
 //
 // CTA (persistent, one per SM; tiles (unit, split) of SP pages, static order blockIdx + k*grid):
-//   warp 0         TMA producer: per page one 2-D TMA of the K page and one of the V page
-//                  (16 x D bf16, 128B swizzle) into a ring of S stages; per tile a bulk copy of
-//                  the unit's q rows; prefetches the next tile's plan / page counts.
+//   warp 0         producer: per page one 1-D bulk async copy (TMA engine) of the K page and
+//                  one of the V page (16 x D bf16, contiguous, stored pre-swizzled) into a ring
+//                  of S stages, one lane per page; per tile a bulk copy of the unit's q rows;
+//                  prefetches the next tile's plan / page counts.
 //   warp 1         merge + combine: merges the consumers' per-tile softmax states (smem),
 //                  publishes the tile's split-K partial, and for a unit's last split runs
 //                  a5-a7.  Never consumes ring stages, so its latency does not stall HBM.
@@ -40,6 +41,15 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// 1-D bulk copy with an L2 eviction-policy hint (KV pages: evict-first, read once per step)
+__device__ __forceinline__ void bulk_load_hint(uint32_t dst, const void* src, uint32_t bytes,
+                                               uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ float lds_f32(uint32_t a) {
@@ -175,12 +185,11 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
 
 template <int D, int NC, int S>
 __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
-    raas_decode_kernel(const __grid_constant__ DecodeParams p,
-                       const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV) {
+    raas_decode_kernel(const __grid_constant__ DecodeParams p) {
   static_assert(D == 64 || D == 128, "head_dim");
   using Lay = DecodeLayout<D, NC, S>;
-  constexpr int KS = Lay::KS, HALVES = D / 64, TILE = Lay::TILE, STAGE = Lay::STAGE;
+  constexpr int KS = Lay::KS, TILE = Lay::TILE, STAGE = Lay::STAGE;
+  constexpr int ROW = 2 * D;  // bytes per token row
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -208,8 +217,6 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       mbar_init(tfree(par), 1);
     }
     fence_mbar_init();
-    tma_prefetch_desc(&tmK);
-    tma_prefetch_desc(&tmV);
   }
   __syncthreads();
   pdl_wait();  // everything above overlapped the previous kernel; state reads start here
@@ -251,26 +258,30 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
         if (n < NC) mbar_arrive_cnt(mfull(par), NC - n);  // warps with no page in this tile
       }
-      for (int i = 0; i < n; ++i, ++j) {
-        const int s = (int)(j % S);
-        const int page = p0 + i;
-        const int c = __shfl_sync(0xffffffffu, cntv, i);
-        mbar_wait(empty(s), ((j / S) & 1) ^ 1);
-        if (lane == 0) {
+      // pages in batches of up to 32, one lane per page: each lane waits for its stage, fills
+      // the stage info and issues two 1-D bulk copies (the K and the V page, 16*D*2 bytes each,
+      // stored pre-swizzled in HBM so they land bank-conflict-free for ldmatrix)
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const int nb = min(32, n - i0);
+        const int c = __shfl_sync(0xffffffffu, cntv, (i0 + lane) & 31);
+        if (lane < nb) {
+          const int i = i0 + lane;
+          const uint32_t jj = j + lane;
+          const int s = (int)(jj % S);
+          const int page = p0 + i;
+          mbar_wait(empty(s), ((jj / S) & 1) ^ 1);
           const bool is_slot = page == slot;
           sinfo[2 * s] = make_int4(unit, page, is_slot ? off + 1 : c, is_slot ? off : -1);
           sinfo[2 * s + 1] =
               make_int4(k, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
           mbar_arrive_expect_tx(full(s), STAGE);
-          const int32_t y = (unit * C + page) * PAGE;
-          const uint32_t dk = ring + s * STAGE, dv = dk + TILE;
-#pragma unroll
-          for (int hf = 0; hf < HALVES; ++hf) {
-            tma_load_2d(dk + hf * 2048, &tmK, hf * 64, y, full(s), pol);
-            tma_load_2d(dv + hf * 2048, &tmV, hf * 64, y, full(s), pol);
-          }
+          const size_t e0 = (size_t)(unit * C + page) * PAGE * D;
+          const uint32_t dk = ring + s * STAGE;
+          bulk_load_hint(dk, p.kstore + e0, TILE, full(s), pol);
+          bulk_load_hint(dk + TILE, p.vstore + e0, TILE, full(s), pol);
         }
         __syncwarp();
+        j += nb;
       }
       ++k;
     }
@@ -390,13 +401,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           const int ch = isv ? lane - NCH : lane;
           const uint4 val = __ldg(reinterpret_cast<const uint4*>(
                                       (isv ? p.v_new : p.k_new) + (size_t)unit * D) + ch);
-          const uint32_t sa = (isv ? vb : kb) + (ch >> 3) * 2048 + patch * 128 +
-                              (((ch & 7) ^ (patch & 7)) << 4);
+          const int phys = ch ^ (patch & 7);  // pre-swizzled page layout (see raas_kernels.cuh)
+          const uint32_t sa = (isv ? vb : kb) + patch * ROW + (phys << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa), "r"(val.x),
                        "r"(val.y), "r"(val.z), "r"(val.w)
                        : "memory");
           *reinterpret_cast<uint4*>((isv ? p.vstore : p.kstore) +
-                                    ((size_t)(unit * C + page) * PAGE + patch) * D + ch * 8) = val;
+                                    ((size_t)(unit * C + page) * PAGE + patch) * D + phys * 8) = val;
           fence_proxy_async_smem();  // before the stage is refilled by TMA
         }
         __syncwarp();
@@ -405,12 +416,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       // ---- a3/a4: S^T = K_page Q^T (M = 16 tokens, N = 8 heads, K = D) ----
       float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
       {
-        const uint32_t krow = kb + (ri + 8 * (mi & 1)) * 128;
+        const uint32_t krow = kb + (ri + 8 * (mi & 1)) * ROW;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           uint32_t a[4];
-          const int chunk = 2 * (ks & 3) + (mi >> 1);
-          ldsm_x4(krow + (ks >> 2) * 2048 + ((chunk ^ ri) << 4), a);
+          const int chunk = 2 * ks + (mi >> 1);
+          ldsm_x4(krow + ((chunk ^ ri) << 4), a);
           if (ks & 1) mma_bf16_16816(c1, a, qb[ks][0], qb[ks][1]);
           else        mma_bf16_16816(c0, a, qb[ks][0], qb[ks][1]);
         }
@@ -449,12 +460,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       const uint32_t b0 = movmatrix_t(pack_bf16x2(p0, p1));
       const uint32_t b1 = movmatrix_t(pack_bf16x2(p2, p3));
       {
-        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * 128;
+        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * ROW;
 #pragma unroll
         for (int mt = 0; mt < KS; ++mt) {
           uint32_t a[4];
-          const int chunk = 2 * (mt & 3) + (mi & 1);
-          ldsm_x4_t(vrow + (mt >> 2) * 2048 + ((chunk ^ ri) << 4), a);
+          const int chunk = 2 * mt + (mi & 1);
+          ldsm_x4_t(vrow + ((chunk ^ ri) << 4), a);
           mma_bf16_16816(acc[mt], a, b0, b1);
         }
       }

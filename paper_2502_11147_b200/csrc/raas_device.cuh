@@ -1,8 +1,7 @@
 // raas_device.cuh — sm_100a PTX helpers used by the libraas kernels.
-// (TMA bulk tensor copies + mbarriers, ldmatrix / movmatrix, bf16 mma.sync, PDL.)
+// (mbarriers, bulk-copy fences, ldmatrix / movmatrix, bf16 mma.sync, PDL.)
 #pragma once
 #include <cstdint>
-#include <cuda.h>
 #include <cuda_bf16.h>
 
 namespace raas {
@@ -38,18 +37,6 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
-}
-__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-}
-// 2-D tile load global -> shared, completion counted on `bar` (bytes), L2 hint `pol`.
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* m, int32_t x,
-                                           int32_t y, uint32_t bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::"
-      "cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(bar), "l"(pol)
-      : "memory");
 }
 // order this thread's generic-proxy smem writes before later async-proxy (TMA) accesses
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -10,7 +10,9 @@
 // Paper: page-based RaaS, §3.3 :143-151, App. B :358-398; readings D1-D20 in DESIGN.md.
 //
 // Data layout (one handle = one layer, `units` = batch * n_kv_heads):
-//   K, V store   [units][C][16][D] bf16           (a page = 16*D*2 contiguous bytes)
+//   K, V store   [units][C][16][D] bf16           (a page = 16*D*2 contiguous bytes; inside a
+//                token row the 16-byte chunk c is stored at chunk c ^ (row & 7), so a linear
+//                bulk copy of the page lands in shared memory bank-conflict-free for ldmatrix)
 //   ts, start, cnt [units][C] int32; npin[units]; plan[units] int4 = {slot, off | evict<<16,
 //   used_eff, t} describing the NEXT step (computed at the end of the previous one).
 //   pmax [units][C][g] fp32 (log2-domain page-max logits), part_ml [units][nsplit][g] float2,
@@ -100,14 +102,15 @@ __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % NCH);
-    const size_t row = i / NCH;  // unit * P + j
-    const int j = (int)(row % P);
-    const size_t u = row / P;
-    const size_t dst = ((u * C + j / PAGE) * PAGE + (j % PAGE)) * D + ch * 8;
+    const size_t src = i / NCH;  // unit * P + j
+    const int j = (int)(src % P);
+    const size_t u = src / P;
+    const int r = j % PAGE;
+    const size_t dst = ((u * C + j / PAGE) * PAGE + r) * D + (ch ^ (r & 7)) * 8;
     *reinterpret_cast<uint4*>(kstore + dst) =
-        __ldg(reinterpret_cast<const uint4*>(k + row * D) + ch);
+        __ldg(reinterpret_cast<const uint4*>(k + src * D) + ch);
     *reinterpret_cast<uint4*>(vstore + dst) =
-        __ldg(reinterpret_cast<const uint4*>(v + row * D) + ch);
+        __ldg(reinterpret_cast<const uint4*>(v + src * D) + ch);
   }
 }
 

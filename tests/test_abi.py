@@ -37,7 +37,7 @@ def test_header_symbols_exported(L):
     assert exported == names
 
 
-def test_sass_is_sm100a_and_uses_tma_and_tensor_cores(L):
+def test_sass_is_sm100a_and_uses_bulk_copies_and_tensor_cores(L):
     cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
     if not os.path.exists(cuobjdump) and not shutil.which("cuobjdump"):
         pytest.skip("no cuobjdump")
@@ -45,7 +45,7 @@ def test_sass_is_sm100a_and_uses_tma_and_tensor_cores(L):
 
     sass = subprocess.run([cuobjdump, "-sass", raas.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in sass
-    assert "UTMALDG" in sass            # TMA tile loads of the KV pages
+    assert "UBLKCP" in sass             # bulk async copies (TMA engine) of the KV pages
     assert "HMMA.16816.F32.BF16" in sass  # bf16 tensor-core MMAs (QK^T and PV)
     assert "LDSM" in sass and "MOVM" in sass
 

@@ -293,3 +293,25 @@ def test_full_size_sampled_units_lockstep(oracle_mod, B, Hq, Hkv, L, P):
     assert worst <= OUT_TOL
     assert band == 0
     assert layer.raas_get_status() == 0
+
+
+def test_kv_store_roundtrip_logical_layout():
+    """raas_get_kv / raas_set_state speak the logical [units][C][16][D] layout even though the
+    device store is chunk-swizzled: prefill -> get_kv reproduces the prompt's K/V, and a
+    set_state(k_store) -> get_kv round trip is the identity."""
+    B, Hq, Hkv, d, P, L = 2, 8, 2, 128, 40, 128
+    st = gaussian_stream(31, B, Hq, Hkv, d, P, 1)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+    k, v = layer.raas_get_kv()
+    U, C = B * Hkv, L // PAGE
+    flat_k = k.reshape(U, C * PAGE, d)[:, :P]
+    flat_v = v.reshape(U, C * PAGE, d)[:, :P]
+    assert np.array_equal(flat_k, st.k_pre.reshape(U, P, d))
+    assert np.array_equal(flat_v, st.v_pre.reshape(U, P, d))
+    rng = np.random.default_rng(1)
+    ks = rng.integers(0, 1 << 16, (U, C, PAGE, d), dtype=np.uint16)
+    s = layer.raas_get_state()
+    layer.raas_set_state(s["t"], s["ts"], s["start"], s["count"], s["pinned"], ks, ks[::-1].copy())
+    k2, v2 = layer.raas_get_kv()
+    assert np.array_equal(k2, ks) and np.array_equal(v2, ks[::-1])
