@@ -74,8 +74,8 @@ typedef struct {
                             request sharding. */
 } raas_config;
 
-/* Bytes of device memory the handle needs (KV store [units][L/16][16][head_dim] bf16 for K and
- * V, int32 page metadata, L2-resident split-K workspace, staging for raas_decode_step_host).
+/* Bytes of device memory the handle needs (KV store: per unit L/16 pages, each 16 K rows + 16 V
+ * rows of head_dim bf16, int32 page metadata, L2-resident split-K workspace, staging for raas_decode_step_host).
  * O(L) per unit, fixed for the life of the handle.  Returns 0 for an invalid config. */
 RAAS_API size_t raas_arena_bytes(const raas_config* cfg);
 

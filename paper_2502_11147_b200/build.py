@@ -10,8 +10,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libraas.so")
 SOURCES = [os.path.join(CSRC, "raas_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("raas_kernels.cuh", "raas_device.cuh")] + [
-    os.path.join(ROOT, "include", "raas.h")]
+def _deps():
+    return SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(ROOT, "include", "raas.h"), os.path.abspath(__file__)]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -31,7 +32,7 @@ def nvcc() -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB):
         mt = os.path.getmtime(LIB)
-        if all(os.path.getmtime(d) <= mt for d in DEPS):
+        if all(os.path.getmtime(d) <= mt for d in _deps()):
             return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *SOURCES, "-o", tmp]

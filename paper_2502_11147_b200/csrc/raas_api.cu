@@ -46,7 +46,7 @@ template <int D>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
-  size_t kstore, vstore, ts, start, cnt, npin, plan, counter, pmax, part_acc, part_ml, status,
+  size_t kvstore, ts, start, cnt, npin, plan, counter, pmax, part_acc, part_ml, status,
       stats, sq, sk, sv, so, total;
 };
 
@@ -89,8 +89,7 @@ Layout layout(const raas_config* c, const Derived& d) {
   const size_t U = d.units, C = d.C, D = c->head_dim, g = d.g;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = up(o + bytes); return r; };
-  L.kstore = take(U * C * raas::PAGE * D * 2);
-  L.vstore = take(U * C * raas::PAGE * D * 2);
+  L.kvstore = take(U * C * 2 * raas::PAGE * D * 2);
   L.ts = take(U * C * 4);
   L.start = take(U * C * 4);
   L.cnt = take(U * C * 4);
@@ -123,16 +122,34 @@ struct DeviceGuard {
   }
 };
 
-// Host view of the KV store is [units][C][16][D] in logical order; on the device each token row
-// keeps its 16-byte chunk c at chunk c ^ (row & 7) (see raas_kernels.cuh).  This permutes a
-// whole store between the two (the permutation is an involution).
-void swizzle_store(const uint16_t* src, uint16_t* dst, size_t pages, int D) {
+// Host view: K and V stores [units][C][16][D] in logical order.  Device store: per page the 16
+// K rows then the 16 V rows, each row keeping its 16-byte chunk c at chunk c ^ (row & 7) (see
+// raas_kernels.cuh).  pack: logical -> device (k or v may be null: that half is left as is);
+// unpack: device -> logical.
+void pack_store(const uint16_t* k, const uint16_t* v, uint16_t* dev, size_t pages, int D) {
   const int nch = D / 8;
   for (size_t pg = 0; pg < pages; ++pg)
-    for (int r = 0; r < raas::PAGE; ++r) {
-      const uint16_t* srow = src + (pg * raas::PAGE + r) * D;
-      uint16_t* drow = dst + (pg * raas::PAGE + r) * D;
-      for (int c = 0; c < nch; ++c) std::memcpy(drow + (c ^ (r & 7)) * 8, srow + c * 8, 16);
+    for (int half = 0; half < 2; ++half) {
+      const uint16_t* src = half ? v : k;
+      if (!src) continue;
+      for (int r = 0; r < raas::PAGE; ++r) {
+        const uint16_t* srow = src + (pg * raas::PAGE + r) * D;
+        uint16_t* drow = dev + ((pg * 2 + half) * raas::PAGE + r) * D;
+        for (int c = 0; c < nch; ++c) std::memcpy(drow + (c ^ (r & 7)) * 8, srow + c * 8, 16);
+      }
+    }
+}
+void unpack_store(const uint16_t* dev, uint16_t* k, uint16_t* v, size_t pages, int D) {
+  const int nch = D / 8;
+  for (size_t pg = 0; pg < pages; ++pg)
+    for (int half = 0; half < 2; ++half) {
+      uint16_t* dst = half ? v : k;
+      if (!dst) continue;
+      for (int r = 0; r < raas::PAGE; ++r) {
+        const uint16_t* srow = dev + ((pg * 2 + half) * raas::PAGE + r) * D;
+        uint16_t* drow = dst + (pg * raas::PAGE + r) * D;
+        for (int c = 0; c < nch; ++c) std::memcpy(drow + c * 8, srow + (c ^ (r & 7)) * 8, 16);
+      }
     }
 }
 
@@ -161,8 +178,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.k_new = static_cast<const __nv_bfloat16*>(k_new);
   p.v_new = static_cast<const __nv_bfloat16*>(v_new);
   p.out = static_cast<__nv_bfloat16*>(out);
-  p.kstore = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kstore);
-  p.vstore = reinterpret_cast<__nv_bfloat16*>(a + h->lay.vstore);
+  p.kvstore = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kvstore);
   p.ts = reinterpret_cast<int32_t*>(a + h->lay.ts);
   p.start = reinterpret_cast<int32_t*>(a + h->lay.start);
   p.cnt = reinterpret_cast<int32_t*>(a + h->lay.cnt);
@@ -292,18 +308,17 @@ int raas_prefill(raas_handle* h, const void* k, const void* v, int32_t P, void* 
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* a = h->arena;
-  auto* ks = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kstore);
-  auto* vs = reinterpret_cast<__nv_bfloat16*>(a + h->lay.vstore);
+  auto* kvs = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kvstore);
   if (P > 0) {
     const size_t total = (size_t)h->d.units * P * (h->cfg.head_dim / 8);
     const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)h->num_sms * 16);
     if (h->cfg.head_dim == 128)
       raas::raas_prefill_copy<128><<<blocks, 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), ks, vs,
+          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs,
           h->d.units, P, h->d.C);
     else
       raas::raas_prefill_copy<64><<<blocks, 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), ks, vs,
+          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs,
           h->d.units, P, h->d.C);
     RAAS_CUDA(cudaGetLastError());
   }
@@ -412,17 +427,17 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.cnt, count, U * C * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.npin, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.plan, plan.data(), U * 16, cudaMemcpyHostToDevice, st));
-  const size_t kvb = U * C * raas::PAGE * h->cfg.head_dim * 2;
-  std::vector<uint16_t> ksw, vsw;
-  if (k_store_host) {
-    ksw.resize(kvb / 2);
-    swizzle_store(static_cast<const uint16_t*>(k_store_host), ksw.data(), U * C, h->cfg.head_dim);
-    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kstore, ksw.data(), kvb, cudaMemcpyHostToDevice, st));
-  }
-  if (v_store_host) {
-    vsw.resize(kvb / 2);
-    swizzle_store(static_cast<const uint16_t*>(v_store_host), vsw.data(), U * C, h->cfg.head_dim);
-    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.vstore, vsw.data(), kvb, cudaMemcpyHostToDevice, st));
+  const size_t pages = U * C, D = h->cfg.head_dim;
+  std::vector<uint16_t> dev;
+  if (k_store_host || v_store_host) {
+    dev.resize(pages * 2 * raas::PAGE * D);
+    if (!k_store_host || !v_store_host) {  // keep the half that is not replaced
+      RAAS_CUDA(cudaMemcpyAsync(dev.data(), a + h->lay.kvstore, dev.size() * 2, cudaMemcpyDeviceToHost, st));
+      RAAS_CUDA(cudaStreamSynchronize(st));
+    }
+    pack_store(static_cast<const uint16_t*>(k_store_host), static_cast<const uint16_t*>(v_store_host),
+               dev.data(), pages, (int)D);
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kvstore, dev.data(), dev.size() * 2, cudaMemcpyHostToDevice, st));
   }
   int rc = refresh(h, st);
   if (rc) return rc;
@@ -436,16 +451,11 @@ int raas_get_kv(raas_handle* h, void* k_store_host, void* v_store_host, void* st
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t pages = (size_t)h->d.units * h->d.C;
-  const size_t kvb = pages * raas::PAGE * h->cfg.head_dim * 2;
-  std::vector<uint16_t> tmp(kvb / 2);
-  void* outs[2] = {k_store_host, v_store_host};
-  const size_t offs[2] = {h->lay.kstore, h->lay.vstore};
-  for (int i = 0; i < 2; ++i) {
-    if (!outs[i]) continue;
-    RAAS_CUDA(cudaMemcpyAsync(tmp.data(), h->arena + offs[i], kvb, cudaMemcpyDeviceToHost, st));
-    RAAS_CUDA(cudaStreamSynchronize(st));
-    swizzle_store(tmp.data(), static_cast<uint16_t*>(outs[i]), pages, h->cfg.head_dim);
-  }
+  std::vector<uint16_t> dev(pages * 2 * raas::PAGE * h->cfg.head_dim);
+  RAAS_CUDA(cudaMemcpyAsync(dev.data(), h->arena + h->lay.kvstore, dev.size() * 2, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaStreamSynchronize(st));
+  unpack_store(dev.data(), static_cast<uint16_t*>(k_store_host), static_cast<uint16_t*>(v_store_host),
+               pages, h->cfg.head_dim);
   return RAAS_OK;
 }
 

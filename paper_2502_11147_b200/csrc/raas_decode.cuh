@@ -11,14 +11,16 @@
 // PAPER.md §3.3 :143-151, App. B :358-398; readings D1-D20 in DESIGN.md.
 //
 // CTA (persistent, one per SM; tiles (unit, split) of SP pages, static order blockIdx + k*grid):
-//   warp 0         producer: per page one 1-D bulk async copy (TMA engine) of the K page and
-//                  one of the V page (16 x D bf16, contiguous, stored pre-swizzled) into a ring
-//                  of S stages, one lane per page; per tile a bulk copy of the unit's q rows;
+//   warp 0         producer: per page ONE 1-D bulk async copy (TMA engine) of the page's K and
+//                  V rows (2 x 16 x D bf16, contiguous, stored pre-swizzled) into a ring of S
+//                  stages, one lane per page; per tile a bulk copy of the unit's q rows;
 //                  prefetches the next tile's plan / page counts.
-//   warp 1         merge + combine: merges the consumers' per-tile softmax states (smem),
-//                  publishes the tile's split-K partial, and for a unit's last split runs
-//                  a5-a7.  Never consumes ring stages, so its latency does not stall HBM.
-//   warps 2..NC+1  consumers: ring position j goes to consumer j % NC; per page
+//   warp 1         merge: merges the consumers' per-tile softmax states (smem), publishes the
+//                  tile's split-K partial (release/acquire counter per unit) and queues a unit
+//                  whose last split it published.
+//   warp 2         combine: a5-a7 for each queued unit.  Neither warp consumes ring stages, so
+//                  their latency does not stall HBM.
+//   warps 3..NC+2  consumers: ring position j goes to consumer j % NC; per page
 //                  S^T = K_page Q^T and O^T += V_page^T P^T on mma.sync m16n8k16 (16 tokens = M,
 //                  the <= 8 q-heads of the GQA group = N), online softmax in fp32 registers.
 #pragma once
@@ -52,6 +54,14 @@ __device__ __forceinline__ void bulk_load_hint(uint32_t dst, const void* src, ui
       "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ float lds_f32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -81,11 +91,14 @@ struct DecodeLayout {
   static constexpr int SCR = MAX_SPLITS * MAX_GROUP * 8 + 2 * MAX_GROUP * 4;
   static constexpr int OFF_SINFO = OFF_SCR + SCR;                          // int4[2] per stage
   static constexpr int OFF_TINFO = OFF_SINFO + S * 32;                     // int4[2] per parity
-  static constexpr int OFF_BAR = OFF_TINFO + 2 * 32;
-  static constexpr int NBAR = 2 * S + 6;  // full[S], empty[S], qfull[2], mfull[2], tfree[2]
+  static constexpr int CQ = 8;                                             // combine queue
+  static constexpr int OFF_CQ = OFF_TINFO + 2 * 32;                         // int[CQ] unit ids
+  static constexpr int OFF_BAR = OFF_CQ + CQ * 4 + 32;
+  // full[S], empty[S], qfull[2], mfull[2], tfree[2], cq_full[CQ], cq_empty[CQ]
+  static constexpr int NBAR = 2 * S + 6 + 2 * CQ;
   static constexpr int BYTES = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = BYTES + 1024;  // + alignment slack
-  static constexpr int THREADS = (NC + 2) * 32;
+  static constexpr int THREADS = (NC + 3) * 32;  // producer, merge, combine, NC consumers
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -198,12 +211,16 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
   const uint32_t merge = base + Lay::OFF_MERGE, scr = base + Lay::OFF_SCR;
   int4* sinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_SINFO);
   int4* tinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_TINFO);
+  volatile int* cq = reinterpret_cast<volatile int*>(smem_raw + (base - raw) + Lay::OFF_CQ);
+  constexpr int CQ = Lay::CQ;
   const uint32_t bar = base + Lay::OFF_BAR;
   auto full = [&](int s) { return bar + 8 * s; };
   auto empty = [&](int s) { return bar + 8 * (S + s); };
   auto qfull = [&](int par) { return bar + 8 * (2 * S + par); };
   auto mfull = [&](int par) { return bar + 8 * (2 * S + 2 + par); };
   auto tfree = [&](int par) { return bar + 8 * (2 * S + 4 + par); };
+  auto cqfull = [&](int q) { return bar + 8 * (2 * S + 6 + q); };
+  auto cqempty = [&](int q) { return bar + 8 * (2 * S + 6 + CQ + q); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -215,6 +232,10 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       mbar_init(qfull(par), 1);
       mbar_init(mfull(par), NC);
       mbar_init(tfree(par), 1);
+    }
+    for (int q = 0; q < CQ; ++q) {
+      mbar_init(cqfull(q), 1);
+      mbar_init(cqempty(q), 1);
     }
     fence_mbar_init();
   }
@@ -258,11 +279,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
         if (n < NC) mbar_arrive_cnt(mfull(par), NC - n);  // warps with no page in this tile
       }
-      // pages in batches of up to 32, one lane per page: each lane waits for its stage, fills
-      // the stage info and issues two 1-D bulk copies (the K and the V page, 16*D*2 bytes each,
-      // stored pre-swizzled in HBM so they land bank-conflict-free for ldmatrix)
-      for (int i0 = 0; i0 < n; i0 += 32) {
-        const int nb = min(32, n - i0);
+      // pages in batches, one lane per page: each lane waits for its stage, fills the stage
+      // info and issues one 1-D bulk copy of the page (K rows then V rows, 16*D*4 contiguous
+      // bytes, stored pre-swizzled in HBM so they land bank-conflict-free for ldmatrix).  A batch never spans
+      // more than S positions: a parity wait must be at most one phase ahead of its barrier.
+      constexpr int BATCH = S < 32 ? S : 32;
+      for (int i0 = 0; i0 < n; i0 += BATCH) {
+        const int nb = min(BATCH, n - i0);
         const int c = __shfl_sync(0xffffffffu, cntv, (i0 + lane) & 31);
         if (lane < nb) {
           const int i = i0 + lane;
@@ -275,10 +298,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           sinfo[2 * s + 1] =
               make_int4(k, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
           mbar_arrive_expect_tx(full(s), STAGE);
-          const size_t e0 = (size_t)(unit * C + page) * PAGE * D;
-          const uint32_t dk = ring + s * STAGE;
-          bulk_load_hint(dk, p.kstore + e0, TILE, full(s), pol);
-          bulk_load_hint(dk + TILE, p.vstore + e0, TILE, full(s), pol);
+          bulk_load_hint(ring + s * STAGE, p.kvstore + (size_t)(unit * C + page) * 2 * PAGE * D,
+                         STAGE, full(s), pol);
         }
         __syncwarp();
         j += nb;
@@ -301,13 +322,27 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       mbar_arrive_cnt(mfull(par), NC);
     }
   } else if (warp == 1) {
-    // ====================== merge (per tile) + combine (per unit) ======================
+    // ============================ merge (per tile) ============================
     const int r = lane >> 2, qd = lane & 3;
+    int npush = 0;
+    auto push = [&](int unit) {  // hand a finished unit (or -1 = END) to the combine warp
+      const int q = npush % CQ;
+      mbar_wait(cqempty(q), ((npush / CQ) & 1) ^ 1);
+      if (lane == 0) {
+        cq[q] = unit;
+        mbar_arrive(cqfull(q));
+      }
+      __syncwarp();
+      ++npush;
+    };
     for (int k = 0;; ++k) {
       const int par = k & 1;
       mbar_wait(mfull(par), (k >> 1) & 1);
       const int4 t0 = tinfo[2 * par], t1 = tinfo[2 * par + 1];
-      if (t1.y & FLAG_END) break;
+      if (t1.y & FLAG_END) {
+        push(-1);
+        break;
+      }
       const int unit = t0.x, split = t0.y, nse = t0.z, n = t0.w, J = t1.x;
       const int nw = min(n, NC);
       float acc[KS * 4];
@@ -348,19 +383,27 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         if (2 * qd < g) { pa0[16 * mt] = acc[4 * mt + 0]; pa0[16 * mt + 8] = acc[4 * mt + 2]; }
         if (2 * qd + 1 < g) { pa1[16 * mt] = acc[4 * mt + 1]; pa1[16 * mt + 8] = acc[4 * mt + 3]; }
       }
-      __threadfence();
       __syncwarp();
-      int old = 0;
-      if (lane == 0) old = atomicAdd(p.counter + unit, 1);
+      int old = 0;  // release our partial / acquire the others' (gpu scope, cumulative)
+      if (lane == 0) old = atom_add_acq_rel_gpu(p.counter + unit, 1);
       old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == nse - 1) {  // this was the unit's last split
-        __threadfence();
-        combine_unit<D>(p, unit, scr, lane);
-      }
+      if (old == nse - 1) push(unit);  // this was the unit's last split
+    }
+  } else if (warp == 2) {
+    // ============================ combine (per unit) ============================
+    for (int i = 0;; ++i) {
+      const int q = i % CQ;
+      mbar_wait(cqfull(q), (i / CQ) & 1);
+      const int unit = cq[q];
+      if (unit < 0) break;
+      fence_acq_rel_gpu();  // the unit's partials from other SMs, as acquired by the merge warp
+      combine_unit<D>(p, unit, scr, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cqempty(q));
     }
   } else {
     // ================================ consumers ================================
-    const int w = warp - 2;
+    const int w = warp - 3;
     const int r = lane >> 2, qd = lane & 3;   // C-fragment row (token) / column pair (head)
     const int mi = lane >> 3, ri = lane & 7;  // ldmatrix matrix / row supplied by this lane
     float acc[KS][4];
@@ -406,8 +449,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa), "r"(val.x),
                        "r"(val.y), "r"(val.z), "r"(val.w)
                        : "memory");
-          *reinterpret_cast<uint4*>((isv ? p.vstore : p.kstore) +
-                                    ((size_t)(unit * C + page) * PAGE + patch) * D + phys * 8) = val;
+          *reinterpret_cast<uint4*>(p.kvstore + ((size_t)(unit * C + page) * 2 * PAGE +
+                                                 (isv ? PAGE : 0) + patch) * D + phys * 8) = val;
           fence_proxy_async_smem();  // before the stage is refilled by TMA
         }
         __syncwarp();

@@ -10,9 +10,10 @@
 // Paper: page-based RaaS, §3.3 :143-151, App. B :358-398; readings D1-D20 in DESIGN.md.
 //
 // Data layout (one handle = one layer, `units` = batch * n_kv_heads):
-//   K, V store   [units][C][16][D] bf16           (a page = 16*D*2 contiguous bytes; inside a
-//                token row the 16-byte chunk c is stored at chunk c ^ (row & 7), so a linear
-//                bulk copy of the page lands in shared memory bank-conflict-free for ldmatrix)
+//   KV store     [units][C][2][16][D] bf16: a page is its 16 K rows followed by its 16 V rows,
+//                16*D*4 contiguous bytes moved by ONE bulk copy; inside a token row the 16-byte
+//                chunk c is stored at chunk c ^ (row & 7), so the copy lands in shared memory
+//                bank-conflict-free for ldmatrix)
 //   ts, start, cnt [units][C] int32; npin[units]; plan[units] int4 = {slot, off | evict<<16,
 //   used_eff, t} describing the NEXT step (computed at the end of the previous one).
 //   pmax [units][C][g] fp32 (log2-domain page-max logits), part_ml [units][nsplit][g] float2,
@@ -31,8 +32,7 @@ struct DecodeParams {
   const __nv_bfloat16* k_new;  // [units][D]
   const __nv_bfloat16* v_new;
   __nv_bfloat16* out;          // [units*g][D]
-  __nv_bfloat16* kstore;
-  __nv_bfloat16* vstore;
+  __nv_bfloat16* kvstore;      // [units][C][2][16][D], chunk-swizzled rows
   int32_t* ts;
   int32_t* start;
   int32_t* cnt;
@@ -95,8 +95,8 @@ namespace raas {
 // ===========================================================================================
 template <int D>
 __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
-                                  const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kstore,
-                                  __nv_bfloat16* vstore, int units, int P, int C) {
+                                  const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kvstore,
+                                  int units, int P, int C) {
   constexpr int NCH = D / 8;
   const size_t total = (size_t)units * P * NCH;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -106,10 +106,10 @@ __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
     const int j = (int)(src % P);
     const size_t u = src / P;
     const int r = j % PAGE;
-    const size_t dst = ((u * C + j / PAGE) * PAGE + r) * D + (ch ^ (r & 7)) * 8;
-    *reinterpret_cast<uint4*>(kstore + dst) =
+    const size_t dst = ((u * C + j / PAGE) * 2 * PAGE + r) * D + (ch ^ (r & 7)) * 8;
+    *reinterpret_cast<uint4*>(kvstore + dst) =
         __ldg(reinterpret_cast<const uint4*>(k + src * D) + ch);
-    *reinterpret_cast<uint4*>(vstore + dst) =
+    *reinterpret_cast<uint4*>(kvstore + dst + PAGE * D) =
         __ldg(reinterpret_cast<const uint4*>(v + src * D) + ch);
   }
 }
