@@ -29,17 +29,22 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
-        mt = os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile libraas.so (``defines``/``out`` only for tuning experiments, see scripts/)."""
+    if not force and os.path.exists(out):
+        mt = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= mt for d in _deps()):
-            return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *SOURCES, "-o", tmp]
+            return out
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
+           *[f"-D{d}" for d in defines], *SOURCES, "-o", tmp]
     subprocess.check_call(cmd, cwd=ROOT)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose="-v" in sys.argv,
+                out=outs[0] if outs else LIB, defines=defs))

@@ -38,8 +38,14 @@ size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 // decode kernel shape (B200): one persistent CTA per SM with a TMA producer
 // warp, a merge/combine warp and NC consumer warps sharing a ring of S page stages.
-constexpr int NC = 8;   // consumer (MMA) warps per CTA
-constexpr int S = 16;   // K+V page stages in the ring (8 KiB each at head_dim 128)
+#ifndef RAAS_NC
+#define RAAS_NC 8
+#endif
+#ifndef RAAS_S
+#define RAAS_S 16
+#endif
+constexpr int NC = RAAS_NC;  // consumer (MMA) warps per CTA
+constexpr int S = RAAS_S;    // K+V page stages in the ring (8 KiB each at head_dim 128)
 template <int D>
 using Lay = raas::DecodeLayout<D, NC, S>;
 template <int D>
@@ -488,5 +494,15 @@ int raas_launch_info(const raas_handle* h, int32_t info[5]) {
   info[4] = h->d.nsplit;
   return RAAS_OK;
 }
+
+#ifdef RAAS_DBG_TIMING
+// tuning experiment only (not part of the ABI in include/raas.h): read + clear the cycle counters
+RAAS_API int raas_debug_timing(uint64_t* out, int n) {
+  RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg, sizeof(uint64_t) * n));
+  std::vector<uint64_t> z(1024 * 16, 0);
+  RAAS_CUDA(cudaMemcpyToSymbol(raas::g_raas_dbg, z.data(), z.size() * 8));
+  return RAAS_OK;
+}
+#endif
 
 }  // extern "C"

@@ -27,9 +27,54 @@
 
 namespace raas {
 
+#ifdef RAAS_DBG_TIMING  // tuning experiment: per-CTA cycle accounting of the pipeline waits
+__device__ unsigned long long g_raas_dbg[1024][16];
+__device__ __forceinline__ long long dbg_clock() { return clock64(); }
+__device__ __forceinline__ void dbg_add(int slot, long long t0) {
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_raas_dbg[blockIdx.x][slot], (unsigned long long)(clock64() - t0));
+}
+__device__ __forceinline__ unsigned long long dbg_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#else
+__device__ __forceinline__ unsigned long long dbg_gtimer() { return 0; }
+__device__ __forceinline__ long long dbg_clock() { return 0; }
+__device__ __forceinline__ void dbg_add(int, long long) {}
+#endif
+#define RAAS_TIMED(slot, stmt)          \
+  do {                                  \
+    const long long t0_ = dbg_clock();  \
+    stmt;                               \
+    dbg_add(slot, t0_);                 \
+  } while (0)
+
 constexpr int FLAG_FIRST = 1;  // first page of this tile for the consuming warp
 constexpr int FLAG_LAST = 2;   // last page of this tile for the consuming warp
 constexpr int FLAG_END = 4;    // no more work
+constexpr int FLAG_SKIP = 8;   // padding position (keeps every tile aligned to the NC consumers)
+constexpr int CQ_OWNED = 1 << 30;  // combine-queue tag: all splits were processed by this CTA
+
+// Static, batch-size-independent tile schedule of one CTA.  With G CTAs, CTA b owns the whole
+// units [b*fu, (b+1)*fu), fu = units / G, and their splits are combined inside the CTA; the
+// R = units - fu*G remaining units are "shared": their split tiles are dealt round-robin to all
+// CTAs and processed FIRST, so their cross-CTA combines overlap the streaming of owned units and
+// the end of the kernel only waits for CTA-local combines.
+struct TileSched {
+  int b, G, fu, nsplit, n_shared, n_total, shared_base;
+  __device__ TileSched(int units, int nsplit_, int G_, int b_) : b(b_), G(G_), nsplit(nsplit_) {
+    fu = units / G;
+    const int RT = (units - fu * G) * nsplit;
+    n_shared = b < RT ? (RT - 1 - b) / G + 1 : 0;
+    n_total = n_shared + fu * nsplit;
+    shared_base = fu * G * nsplit;
+  }
+  __device__ int tile(int i, bool& owned) const {
+    owned = i >= n_shared;
+    return owned ? b * fu * nsplit + (i - n_shared) : shared_base + b + i * G;
+  }
+};
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -107,6 +152,8 @@ struct DecodeLayout {
 template <int D>
 __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, uint32_t scr,
                                              int lane) {
+  // Latency-oriented: every phase issues all of its global loads before using any of them, so
+  // a unit costs ~3 dependent L2 round trips (ml; acc + page metadata; stores).
   const int C = p.C, g = p.g, SP = p.split_pages;
   const int4 pl = __ldcg(p.plan + unit);
   const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
@@ -114,73 +161,127 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
   const int npin = __ldg(p.npin + unit);
   const int nse = (used_eff + SP - 1) / SP;
   const int NE = nse * g;
-  const uint32_t scr_ml = scr;                                  // float2[nse][g]
+  const uint32_t scr_w = scr;                                   // float[nse][g] split weights
   const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
   const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
   const float2* ml_g = p.part_ml + (size_t)unit * p.nsplit * g;
-#pragma unroll 4
-  for (int i = lane; i < NE; i += 32) {
-    const float2 ml = __ldcg(ml_g + i);
-    sts_f32(scr_ml + 8 * i, ml.x);
-    sts_f32(scr_ml + 8 * i + 4, ml.y);
+  // ---- a5 (1): split maxima and sums -> per-head LSE and split weights ----
+  for (int i0 = 0; i0 < NE; i0 += 64) {
+    const int ia = i0 + lane, ib = i0 + 32 + lane;
+    const float2 mla = ia < NE ? __ldcg(ml_g + ia) : make_float2(-INFINITY, 0.f);
+    const float2 mlb = ib < NE ? __ldcg(ml_g + ib) : make_float2(-INFINITY, 0.f);
+    if (ia < NE) { sts_f32(scr_w + 8 * ia, mla.x); sts_f32(scr_w + 8 * ia + 4, mla.y); }
+    if (ib < NE) { sts_f32(scr_w + 8 * ib, mlb.x); sts_f32(scr_w + 8 * ib + 4, mlb.y); }
   }
   __syncwarp();
-  if (lane < g) {  // a5: LSE_h = M + log2 sum_s 2^(m_s - M) l_s  (log2 domain)
+  if (lane < g) {  // LSE_h = M + log2 sum_s 2^(m_s - M) l_s   (log2 domain)
     float M = -INFINITY;
-    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_ml + 8 * (s * g + lane)));
+    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_w + 8 * (s * g + lane)));
     float L = 0.f;
     for (int s = 0; s < nse; ++s) {
-      const uint32_t a = scr_ml + 8 * (s * g + lane);
+      const uint32_t a = scr_w + 8 * (s * g + lane);
       const float w = fast_exp2(lds_f32(a) - M);
       L += w * lds_f32(a + 4);
-      sts_f32(a, w);  // keep the split weight in place of m_s
+      sts_f32(a, w);  // the split weight replaces m_s
     }
     sts_f32(scr_lse + 4 * lane, M + log2f(L));
     sts_f32(scr_inv + 4 * lane, 1.f / L);
   }
   __syncwarp();
-  // out[h][d] = sum_s w_s acc_s[h][d] / L_h, 4 dims per chunk
-  constexpr int CPH = D / 4;  // chunks per head
-  const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
-  for (int c = lane; c < g * CPH; c += 32) {
-    const int h = c / CPH, d4 = c - h * CPH;
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-    for (int s = 0; s < nse; ++s) {
-      const float w = lds_f32(scr_ml + 8 * (s * g + h));
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)s * g + h) * D) + d4);
-      o.x += w * v.x; o.y += w * v.y; o.z += w * v.z; o.w += w * v.w;
+  // ---- prefetch the first chunk of page metadata (used by a6/a7 below) ----
+  constexpr int PPL = 4;  // pages per lane per chunk
+  int tsv[PPL], stv[PPL];
+  float pmv[PPL][MAX_GROUP];
+  auto load_meta = [&](int pc) {
+#pragma unroll
+    for (int i = 0; i < PPL; ++i) {
+      const int pg = pc + 32 * i + lane;
+      const bool ok = pg < used_eff;
+      const size_t ix = (size_t)unit * C + pg;
+      tsv[i] = ok ? __ldcg(p.ts + ix) : 0;
+      stv[i] = ok ? __ldcg(p.start + ix) : 0;
+#pragma unroll
+      for (int h = 0; h < MAX_GROUP; ++h)
+        pmv[i][h] = (ok && h < g && pg >= npin) ? __ldcg(p.pmax + ix * g + h) : -INFINITY;
     }
-    const float inv = lds_f32(scr_inv + 4 * h);
-    uint2 pk = make_uint2(pack_bf16x2(o.x * inv, o.y * inv), pack_bf16x2(o.z * inv, o.w * inv));
-    *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) = pk;
+  };
+  load_meta(0);
+  // ---- a5 (2): out[h][d] = sum_s w_s acc_s[h][d] / L_h, float4 chunks ----
+  constexpr int CPH = D / 4;                   // chunks per head
+  constexpr int CPL = MAX_GROUP * CPH / 32;    // chunks per lane (max)
+  constexpr int SG = 2;                        // splits per load group
+  const int nch = g * CPH;
+  const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
+  float4 o[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = 0; s0 < nse; s0 += SG) {
+    float4 v[CPL][SG];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane + 32 * i, h = c / CPH, d4 = c - h * CPH;
+#pragma unroll
+      for (int u = 0; u < SG; ++u)
+        v[i][u] = (c < nch && s0 + u < nse)
+                      ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = lane + 32 * i, h = c / CPH;
+      if (c < nch) {
+#pragma unroll
+        for (int u = 0; u < SG; ++u) {
+          if (s0 + u < nse) {
+            const float w = lds_f32(scr_w + 8 * ((s0 + u) * g + h));
+            o[i].x += w * v[i][u].x; o[i].y += w * v[i][u].y;
+            o[i].z += w * v[i][u].z; o[i].w += w * v[i][u].w;
+          }
+        }
+      }
+    }
   }
-  // a6: stamp; a2 metadata of the write slot; a7 candidates
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int c = lane + 32 * i, h = c / CPH, d4 = c - h * CPH;
+    if (c < nch) {
+      const float inv = lds_f32(scr_inv + 4 * h);
+      const uint2 pk = make_uint2(pack_bf16x2(o[i].x * inv, o[i].y * inv),
+                                  pack_bf16x2(o[i].z * inv, o[i].w * inv));
+      *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) = pk;
+    }
+  }
+  // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
   float lse[MAX_GROUP];
 #pragma unroll
   for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
   Cand best{~0ull, -1};
   int n_stamp = 0, n_dec = 0;
-#pragma unroll 2
-  for (int pg = lane; pg < used_eff; pg += 32) {
-    const size_t ix = (size_t)unit * C + pg;
-    int ts_p = __ldcg(p.ts + ix), st_p = __ldcg(p.start + ix);
-    const bool is_slot = pg == slot;
-    if (is_slot) {
-      if (off == 0) { st_p = t; p.start[ix] = t; }
-      p.cnt[ix] = off + 1;
-    }
-    if (pg >= npin) {
-      float x = -INFINITY;
-      const float* pm = p.pmax + ix * g;
+  for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
+    if (pc > 0) load_meta(pc);
 #pragma unroll
-      for (int h = 0; h < MAX_GROUP; ++h)
-        if (h < g) x = fmaxf(x, __ldcg(pm + h) - lse[h]);
-      const bool stamp = x > p.log2_alpha;  // strict (D3)
-      ++n_dec;
-      n_stamp += stamp ? 1 : 0;
-      if (stamp || is_slot) { ts_p = t; p.ts[ix] = t; }  // stamp, or write refresh (D8)
-      cand_update(best, cand_key(ts_p, st_p), pg);
+    for (int i = 0; i < PPL; ++i) {
+      const int pg = pc + 32 * i + lane;
+      if (pg < used_eff) {
+        const size_t ix = (size_t)unit * C + pg;
+        int ts_p = tsv[i], st_p = stv[i];
+        const bool is_slot = pg == slot;
+        if (is_slot) {
+          if (off == 0) { st_p = t; p.start[ix] = t; }
+          p.cnt[ix] = off + 1;
+        }
+        if (pg >= npin) {
+          float x = -INFINITY;
+#pragma unroll
+          for (int h = 0; h < MAX_GROUP; ++h)
+            if (h < g) x = fmaxf(x, pmv[i][h] - lse[h]);
+          const bool stamp = x > p.log2_alpha;  // strict (D3)
+          ++n_dec;
+          n_stamp += stamp ? 1 : 0;
+          if (stamp || is_slot) { ts_p = t; p.ts[ix] = t; }  // stamp, or write refresh (D8)
+          cand_update(best, cand_key(ts_p, st_p), pg);
+        }
+      }
     }
   }
   const int victim = warp_argmin_page(best);
@@ -242,6 +343,10 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
   __syncthreads();
   pdl_wait();  // everything above overlapped the previous kernel; state reads start here
   pdl_launch_dependents();
+  const long long t_start = dbg_clock();
+#ifdef RAAS_DBG_TIMING
+  if (threadIdx.x == 0) g_raas_dbg[blockIdx.x][12] = dbg_gtimer();
+#endif
 
   const int C = p.C, SP = p.split_pages, g = p.g;
   const int n_tiles = p.units * p.nsplit;
@@ -258,23 +363,39 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         ncnt = (lane < SP && q0 + lane < C) ? p.cnt[(size_t)u * C + q0 + lane] : 0;
       }
     };
-    fetch(blockIdx.x);
+    const TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
+    bool owned_next = false;
+    fetch(sched.n_total > 0 ? sched.tile(0, owned_next) : n_tiles);
     uint32_t j = 0;
     int k = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (int ti = 0; ti < sched.n_total; ++ti) {
+      bool owned;
+      const int tile = sched.tile(ti, owned);
       const int unit = tile / p.nsplit, split = tile - unit * p.nsplit;
       const int4 pl = nplan;
       const int cntv = ncnt;
-      fetch(tile + gridDim.x);  // next tile's metadata, in flight while this tile is issued
+      // next tile's metadata, in flight while this tile is issued
+      fetch(ti + 1 < sched.n_total ? sched.tile(ti + 1, owned_next) : n_tiles);
       const int used_eff = pl.z, p0 = split * SP;
       const int n = min(p0 + SP, used_eff) - p0;
       if (n <= 0) continue;  // pages not yet allocated (fill phase)
       const int slot = pl.x, off = pl.y & 0xffff;
+      // align the tile to the consumer count: page i of a tile is always consumed by warp
+      // i % NC, so the split's arithmetic does not depend on the schedule (determinism)
+      for (; j % NC != 0; ++j) {
+        const int s = (int)(j % S);
+        mbar_wait(empty(s), ((j / S) & 1) ^ 1);
+        if (lane == 0) {
+          sinfo[2 * s + 1] = make_int4(0, FLAG_SKIP, 0, 0);
+          mbar_arrive(full(s));
+        }
+        __syncwarp();
+      }
       const int par = k & 1;
-      mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1);  // tile k-2 merged: its q/info/deposits free
+      RAAS_TIMED(0, mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1));  // tile k-2 merged: slots free
       if (lane == 0) {
         tinfo[2 * par] = make_int4(unit, split, (used_eff + SP - 1) / SP, n);
-        tinfo[2 * par + 1] = make_int4((int)j, 0, 0, 0);
+        tinfo[2 * par + 1] = make_int4((int)j, 0, owned ? 1 : 0, 0);
         mbar_arrive_expect_tx(qfull(par), g * D * 2);
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
         if (n < NC) mbar_arrive_cnt(mfull(par), NC - n);  // warps with no page in this tile
@@ -292,7 +413,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           const uint32_t jj = j + lane;
           const int s = (int)(jj % S);
           const int page = p0 + i;
-          mbar_wait(empty(s), ((jj / S) & 1) ^ 1);
+          RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
           const bool is_slot = page == slot;
           sinfo[2 * s] = make_int4(unit, page, is_slot ? off + 1 : c, is_slot ? off : -1);
           sinfo[2 * s + 1] =
@@ -321,13 +442,17 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       tinfo[2 * par + 1] = make_int4(0, FLAG_END, 0, 0);
       mbar_arrive_cnt(mfull(par), NC);
     }
+    dbg_add(8, t_start);
+#ifdef RAAS_DBG_TIMING
+    if (lane == 0) g_raas_dbg[blockIdx.x][13] = dbg_gtimer();
+#endif
   } else if (warp == 1) {
     // ============================ merge (per tile) ============================
     const int r = lane >> 2, qd = lane & 3;
     int npush = 0;
     auto push = [&](int unit) {  // hand a finished unit (or -1 = END) to the combine warp
       const int q = npush % CQ;
-      mbar_wait(cqempty(q), ((npush / CQ) & 1) ^ 1);
+      RAAS_TIMED(7, mbar_wait(cqempty(q), ((npush / CQ) & 1) ^ 1));
       if (lane == 0) {
         cq[q] = unit;
         mbar_arrive(cqfull(q));
@@ -337,13 +462,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     };
     for (int k = 0;; ++k) {
       const int par = k & 1;
-      mbar_wait(mfull(par), (k >> 1) & 1);
+      RAAS_TIMED(2, mbar_wait(mfull(par), (k >> 1) & 1));
       const int4 t0 = tinfo[2 * par], t1 = tinfo[2 * par + 1];
       if (t1.y & FLAG_END) {
         push(-1);
         break;
       }
-      const int unit = t0.x, split = t0.y, nse = t0.z, n = t0.w, J = t1.x;
+      const int unit = t0.x, split = t0.y, nse = t0.z, n = t0.w, J = t1.x, owned = t1.z;
       const int nw = min(n, NC);
       float acc[KS * 4];
 #pragma unroll
@@ -384,23 +509,33 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         if (2 * qd + 1 < g) { pa1[16 * mt] = acc[4 * mt + 1]; pa1[16 * mt + 8] = acc[4 * mt + 3]; }
       }
       __syncwarp();
-      int old = 0;  // release our partial / acquire the others' (gpu scope, cumulative)
-      if (lane == 0) old = atom_add_acq_rel_gpu(p.counter + unit, 1);
-      old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == nse - 1) push(unit);  // this was the unit's last split
+      if (owned) {  // every split of the unit is ours and in order: no cross-CTA counter
+        if (split == nse - 1) push(unit | CQ_OWNED);
+      } else {
+        int old = 0;  // release our partial / acquire the others' (gpu scope, cumulative)
+        if (lane == 0) old = atom_add_acq_rel_gpu(p.counter + unit, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == nse - 1) push(unit);  // this was the unit's last split
+      }
     }
+    dbg_add(9, t_start);
   } else if (warp == 2) {
     // ============================ combine (per unit) ============================
     for (int i = 0;; ++i) {
       const int q = i % CQ;
-      mbar_wait(cqfull(q), (i / CQ) & 1);
-      const int unit = cq[q];
-      if (unit < 0) break;
-      fence_acq_rel_gpu();  // the unit's partials from other SMs, as acquired by the merge warp
+      RAAS_TIMED(4, mbar_wait(cqfull(q), (i / CQ) & 1));
+      const int entry = cq[q];
+      if (entry < 0) break;
+      const int unit = entry & (CQ_OWNED - 1);
+      if (!(entry & CQ_OWNED)) fence_acq_rel_gpu();  // partials from other SMs (acquired by merge)
       combine_unit<D>(p, unit, scr, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(cqempty(q));
     }
+    dbg_add(10, t_start);
+#ifdef RAAS_DBG_TIMING
+    if (lane == 0) g_raas_dbg[blockIdx.x][14] = dbg_gtimer();
+#endif
   } else {
     // ================================ consumers ================================
     const int w = warp - 3;
@@ -416,10 +551,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     }
     for (uint32_t j = w;; j += NC) {
       const int s = (int)(j % S);
-      mbar_wait(full(s), (j / S) & 1);
+      RAAS_TIMED(5, mbar_wait(full(s), (j / S) & 1));
       const int4 i0 = sinfo[2 * s], i1 = sinfo[2 * s + 1];
       const int flags = i1.y;
       if (flags & FLAG_END) break;
+      if (flags & FLAG_SKIP) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty(s));
+        continue;
+      }
       const int unit = i0.x, page = i0.y, cnt = i0.z, patch = i0.w, k = i1.x, par = k & 1;
       const uint32_t kb = ring + s * STAGE, vb = kb + TILE;
 
@@ -428,7 +568,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         for (int mt = 0; mt < KS; ++mt) acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
         m0 = m1 = -INFINITY;
         l0 = l1 = 0.f;
-        mbar_wait(qfull(par), (k >> 1) & 1);
+        RAAS_TIMED(6, mbar_wait(qfull(par), (k >> 1) & 1));
         const uint32_t qrow = qbuf + par * Lay::QBUF + r * D * 2 + qd * 4;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
@@ -456,6 +596,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         __syncwarp();
       }
 
+#ifdef RAAS_DBG_NOCOMPUTE  // pipeline-ceiling experiment: consume without computing
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty(s));
+      if (flags & FLAG_LAST) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mfull(par));
+      }
+      continue;
+#endif
       // ---- a3/a4: S^T = K_page Q^T (M = 16 tokens, N = 8 heads, K = D) ----
       float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
       {
@@ -534,6 +683,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         if (lane == 0) mbar_arrive(mfull(par));
       }
     }
+    dbg_add(11, t_start);
   }
 }
 

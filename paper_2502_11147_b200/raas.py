@@ -16,7 +16,8 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libraas.so")
+# RAAS_LIB may point at an alternative build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("RAAS_LIB") or os.path.join(_HERE, "libraas.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "raas.h")
 
 RAAS_OK, RAAS_E_INVALID, RAAS_E_UNSUPPORTED, RAAS_E_STATE, RAAS_E_BUDGET, RAAS_E_CUDA, RAAS_E_ARENA = range(7)

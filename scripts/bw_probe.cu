@@ -38,8 +38,17 @@ __global__ void ldg_stream(const int4* __restrict__ a, size_t n, int* sink) {
 }
 
 // ring: S stages of CH bytes; chunk c of this CTA goes to consumer warp c % NCONS
+// chunk order of CTA b: mode 0 contiguous range; mode 1 tiles of TP chunks round-robin
+// (tile b, b+grid, ...: the decode kernel's static schedule); mode 2 contiguous tile range
+__device__ __forceinline__ size_t chunk_of(int mode, size_t j, size_t c0, int TP) {
+  if (mode == 1) {
+    const size_t t = blockIdx.x + (j / TP) * gridDim.x;
+    return t * TP + j % TP;
+  }
+  return c0 + j;
+}
 template <int NCONS>
-__global__ void ring_stream(const uint8_t* a, size_t nchunks, int CH, int S) {
+__global__ void ring_stream(const uint8_t* a, size_t nchunks, int CH, int S, int mode, int TP) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t base = smem_u32(sm);
   const uint32_t bars = base + S * CH;
@@ -64,7 +73,7 @@ __global__ void ring_stream(const uint8_t* a, size_t nchunks, int CH, int S) {
         const int s = (int)(j % S);
         mbar_wait(bars + 8 * (S + s), ((j / S) & 1) ^ 1);
         mbar_expect(bars + 8 * s, CH);
-        bulk(base + s * CH, a + (c0 + j) * CH, CH, bars + 8 * s, pol);
+        bulk(base + s * CH, a + chunk_of(mode, j, c0, TP) * CH, CH, bars + 8 * s, pol);
       }
       __syncwarp();
     }
@@ -106,18 +115,18 @@ int main() {
     double gbs = timeit([&] { ldg_stream<<<sms * bpsm, 256>>>((const int4*)a, bytes / 16, sink); });
     printf("ldg_stream blocks/SM=%d: %.0f GB/s\n", bpsm, gbs);
   }
-  for (int ch : {4096, 8192, 16384}) {
-    for (int S : {8, 16, 24, 32}) {
-      for (int cps : {1, 2}) {
-        const int smem = S * ch + 2 * S * 8 + 64;
-        if (smem * cps > 220 * 1024) continue;
-        auto k = ring_stream<8>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        double gbs = timeit([&] { k<<<sms * cps, 9 * 32, smem>>>(a, bytes / ch, ch, S); });
-        cudaError_t e = cudaGetLastError();
-        printf("ring chunk=%5d S=%2d CTAs/SM=%d inflight/SM=%4d KB: %.0f GB/s %s\n", ch, S, cps,
-               S * ch * cps / 1024, gbs, e == cudaSuccess ? "" : cudaGetErrorString(e));
-      }
+  for (int mode : {0, 1, 2}) {
+    for (int TP : {32, 31, 64}) {
+      const int ch = 8192, S = 16;
+      const int smem = S * ch + 2 * S * 8 + 64;
+      auto k = ring_stream<8>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      const size_t nch = (bytes / ch) / (TP * sms) * (TP * sms);
+      double gbs = timeit([&] { k<<<sms, 9 * 32, smem>>>(a, nch, ch, S, mode, TP); });
+      gbs *= (double)(nch * ch) / bytes;
+      printf("ring 8K S=16 mode=%d tile=%d chunks: %.0f GB/s %s\n", mode, TP, gbs,
+             cudaGetErrorString(cudaGetLastError()));
+      if (mode != 1) break;
     }
   }
   return 0;

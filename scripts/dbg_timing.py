@@ -1,0 +1,51 @@
+"""Tuning experiment: cycle accounting of the decode pipeline (needs a RAAS_DBG_TIMING build,
+RAAS_LIB=build_exp/libraas_dbg.so).  Config 3 shapes, 1 layer, full-cache state."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import numpy as np, torch
+from paper_2502_11147_b200 import raas
+from paper_2502_11147_b200.raas import RaasLayer
+from paper_2502_11147_b200.synth import random_steady_state
+B, Hq, Hkv, d, P, L = 64, 32, 8, 128, 256, 2048
+C, Pp, U = L // 16, P // 16, B * Hkv
+meta = random_steady_state(77, U, C, Pp, Pp * 16 + 64 * (C - Pp) + 5)
+layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B) for _ in range(8)]
+for ly in layers:
+    ly.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"])
+q = torch.randn(B, Hq, d, device="cuda").bfloat16(); kv = torch.randn(B, Hkv, d, device="cuda").bfloat16()
+out = torch.empty_like(q)
+L_ = raas.lib(); L_.raas_debug_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = np.zeros((1024, 16), np.uint64)
+for i in range(4):
+    for ly in layers: ly.raas_decode_step(q, kv, kv, out)
+torch.cuda.synchronize()
+L_.raas_debug_timing(buf.ctypes.data_as(ctypes.c_void_p), buf.size)
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record()
+N = 16
+for i in range(N):
+    for ly in layers: ly.raas_decode_step(q, kv, kv, out)
+e1.record(); torch.cuda.synchronize()
+L_.raas_debug_timing(buf.ctypes.data_as(ctypes.c_void_p), buf.size)
+ms = e0.elapsed_time(e1) / (N * len(layers))
+g = layers[0].raas_launch_info()["grid"]
+b = buf[:g].astype(np.float64).sum(0) / g / (N * len(layers))
+names = {0: "prod tfree wait", 1: "prod empty wait (lane0)", 8: "prod total", 2: "merge mfull wait",
+         7: "merge cq push wait", 9: "merge total", 4: "combine cq wait", 10: "combine total",
+         5: "consumer full wait (sum 8 warps)", 6: "consumer q wait (sum)", 11: "consumer total (sum)"}
+print(f"launch {ms*1e3:.1f} us  ({537e6/(ms*1e-3)/1e9:.0f} GB/s)")
+for k, n in names.items():
+    print(f"{n:34s} {b[k]:12.0f} cyc/launch/CTA")
+
+# one isolated launch: per-CTA start / producer end / combine end (globaltimer, ns)
+torch.cuda.synchronize()
+L_.raas_debug_timing(buf.ctypes.data_as(ctypes.c_void_p), buf.size)
+layers[0].raas_decode_step(q, kv, kv, out)
+torch.cuda.synchronize()
+L_.raas_debug_timing(buf.ctypes.data_as(ctypes.c_void_p), buf.size)
+st, pe, ce = buf[:g, 12].astype(np.int64), buf[:g, 13].astype(np.int64), buf[:g, 14].astype(np.int64)
+t0 = st.min()
+print("CTA start spread (us): min 0 max %.1f" % ((st.max() - t0) / 1e3))
+print("producer end (us): min %.1f median %.1f max %.1f" % ((pe.min() - t0) / 1e3, np.median(pe - t0) / 1e3, (pe.max() - t0) / 1e3))
+print("combine end  (us): min %.1f median %.1f max %.1f" % ((ce.min() - t0) / 1e3, np.median(ce - t0) / 1e3, (ce.max() - t0) / 1e3))
+print("cycles/ns (SM clock GHz) ~ %.2f" % (buf[:g, 8].astype(np.float64).mean() / np.mean(pe - st)))

@@ -315,3 +315,37 @@ def test_kv_store_roundtrip_logical_layout():
     layer.raas_set_state(s["t"], s["ts"], s["start"], s["count"], s["pinned"], ks, ks[::-1].copy())
     k2, v2 = layer.raas_get_kv()
     assert np.array_equal(k2, ks) and np.array_equal(v2, ks[::-1])
+
+
+def test_request_sharding_bitwise_at_full_size():
+    """Config-3 shapes from a full-cache state: the batch run as one handle (148 CTAs, many
+    tiles each, unit-affine schedule) and as two half-batch handles (different schedules)
+    give bitwise identical outputs and metadata — the split arithmetic is schedule-free."""
+    B, Hq, Hkv, d, L, P = 64, 32, 8, 128, 2048, 256
+    C, Pp, U = L // PAGE, P // PAGE, B * Hkv
+    meta = random_steady_state(5, U, C, Pp, Pp * PAGE + 4 * PAGE * (C - Pp) + 3)
+    rng = np.random.Generator(np.random.Philox(6))
+    kst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
+    vst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
+    steps = [(bf16_bits(2.5 * rng.standard_normal((B, Hq, d), np.float32)),
+              bf16_bits(rng.standard_normal((B, Hkv, d), np.float32)),
+              bf16_bits(rng.standard_normal((B, Hkv, d), np.float32))) for _ in range(20)]
+
+    def run(b0, b1):
+        u0, u1 = b0 * Hkv, b1 * Hkv
+        layer = RaasLayer(L, 1e-4, Hq, Hkv, d, b1 - b0)
+        layer.raas_set_state(meta["t"][u0:u1], meta["ts"][u0:u1], meta["start"][u0:u1],
+                             meta["count"][u0:u1], meta["pinned"][u0:u1], kst[u0:u1], vst[u0:u1])
+        out = torch.empty((b1 - b0, Hq, d), dtype=torch.bfloat16, device="cuda")
+        outs = []
+        for q, k, v in steps:
+            layer.raas_decode_step(to_dev(q[b0:b1]), to_dev(k[b0:b1]), to_dev(v[b0:b1]), out)
+            outs.append(from_dev(out))
+        return np.stack(outs), layer.raas_get_state()
+
+    full, sf = run(0, B)
+    lo, slo = run(0, B // 2)
+    hi, shi = run(B // 2, B)
+    assert np.array_equal(np.concatenate([lo, hi], axis=1), full)
+    for k in ("ts", "start", "count", "t"):
+        assert np.array_equal(np.concatenate([slo[k], shi[k]]), sf[k])
