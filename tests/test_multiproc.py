@@ -1,0 +1,84 @@
+"""world_size-2 gloo tests (CPU) of the multi-GPU host logic: request shards
+partition the batch, head shards keep GQA groups whole, the max-over-ranks timing reduction,
+and the head-sharded output all-gather reassembles [B, Hq, d]."""
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+from paper_2502_11147_b200.shard import gather_heads, head_range, max_over_ranks, request_range  # noqa: E402
+
+
+def test_request_range_partitions():
+    for B in (0, 1, 7, 64, 256):
+        for world in (1, 2, 3, 8):
+            ranges = [request_range(B, world, r) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == B
+            assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in ranges]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_head_range_keeps_groups():
+    for (hkv, hq, world) in ((8, 32, 8), (8, 32, 2), (4, 28, 4), (4, 28, 2)):
+        g = hq // hkv
+        seen = []
+        for r in range(world):
+            kl, kh, ql, qh = head_range(hkv, hq, world, r)
+            assert (qh - ql) == (kh - kl) * g and ql == kl * g
+            seen += list(range(ql, qh))
+        assert seen == list(range(hq))
+    with pytest.raises(ValueError):
+        head_range(4, 28, 8, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # max over ranks
+        m = max_over_ranks(10.0 + rank)
+        # head-sharded gather: each rank holds its heads of a known full tensor
+        B, Hq, d = 3, 8, 4
+        full = torch.arange(B * Hq * d, dtype=torch.float32).reshape(B, Hq, d)
+        _, _, ql, qh = head_range(2, Hq, world, rank)
+        got = gather_heads(full[:, ql:qh].contiguous())
+        ok_gather = torch.equal(got, full)
+        # request shards cover the batch exactly once
+        lo, hi = request_range(64, world, rank)
+        cover = torch.zeros(64, dtype=torch.int64)
+        cover[lo:hi] = 1
+        dist.all_reduce(cover)
+        q.put((rank, m, ok_gather, bool((cover == 1).all())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_collectives():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, m, ok_gather, ok_cover in res:
+        assert m == 11.0
+        assert ok_gather and ok_cover
