@@ -212,13 +212,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     B, hq, hkv, d, L, P, nl = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["d"], cfg["L"], cfg["P"], cfg["layers"]
     g = hq // hkv
+    heads = args.shard == "heads" and world > 1
+    hq_full = hq
+    if heads:  # this rank's kv-heads and their q-heads; out is all-gathered every layer-step
+        from paper_2502_11147_b200.shard import gather_heads, head_range
+
+        kv_lo, kv_hi, q_lo, q_hi = head_range(hkv, hq, world, rank)
+        hkv, hq = kv_hi - kv_lo, q_hi - q_lo
     C = L // 16
     Pp = -(-P // 16)
     units = B * hkv
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * args.config + rank)
-    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=cfg.get("split_pages", 0))
-              for _ in range(nl)]
+    sp = args.split_pages if args.split_pages else cfg.get("split_pages", 0)
+    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp) for _ in range(nl)]
     info = layers[0].raas_launch_info()
     for ly in layers:
         k = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
@@ -230,7 +237,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     ks = [torch.randn((B, hkv, d), device=dev, generator=gen).bfloat16() for _ in range(R)]
     vs = [torch.randn((B, hkv, d), device=dev, generator=gen).bfloat16() for _ in range(R)]
     outs = [torch.empty((B, hq, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)]
+    outs_full = [torch.empty((B, hq_full, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)] if heads else None
     stream = torch.cuda.Stream(device=dev)
+
+    def eager_step(s_):  # head-sharded: decode, then the per-layer NCCL all-gather of out
+        for li, ly in enumerate(layers):
+            ly.raas_decode_step(qs[s_], ks[s_], vs[s_], outs[li], stream=stream)
+            gather_heads(outs[li], outs_full[li])
 
     # one CUDA graph per ring slot, each = one model step (nl decode launches)
     graphs = []
@@ -238,18 +251,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     # steady state before capture: fill the decode pages once, then a further page cycle
     fill_steps = (C - Pp) * 16 + 256 if args.fill < 0 else args.fill
     fill_steps = min(fill_steps, cfg["decode"])
-    with torch.cuda.stream(stream):
-        for s in range(R):
-            gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr, stream=stream):
-                for li, ly in enumerate(layers):
-                    ly.raas_decode_step(qs[s], ks[s], vs[s], outs[li], stream=stream)
-            graphs.append(gr)
+    if not heads:
+        with torch.cuda.stream(stream):
+            for s in range(R):
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=stream):
+                    for li, ly in enumerate(layers):
+                        ly.raas_decode_step(qs[s], ks[s], vs[s], outs[li], stream=stream)
+                graphs.append(gr)
+    run_step = (lambda s_: eager_step(s_)) if heads else (lambda s_: graphs[s_].replay())
     # capturing does not execute; fill now (real steps)
     t_fill = time.perf_counter()
     with torch.cuda.stream(stream):  # CUDAGraph.replay() launches on the current stream
         for i in range(fill_steps):
-            graphs[i % R].replay()
+            run_step(i % R)
     torch.cuda.synchronize()
     t_fill = time.perf_counter() - t_fill
     step0 = fill_steps
@@ -261,7 +276,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # warmup
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            graphs[(step0 + i) % R].replay()
+            run_step((step0 + i) % R)
     step0 += args.warmup
     torch.cuda.synchronize()
     if world > 1:
@@ -274,7 +289,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for i in range(args.steps):
-                graphs[(step0 + i) % R].replay()
+                run_step((step0 + i) % R)
             ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -311,11 +326,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         raise RuntimeError(f"achieved {achieved:.0f} GB/s > 1.3x the copy peak: the timed region "
                            "did not do the work")
     model_steps_per_s = args.steps / (ms_max / 1e3)
-    value = model_steps_per_s * world
+    value = model_steps_per_s * (1 if heads else world)  # head sharding: all ranks, one batch
 
     # ---------------- e2e: through raas_decode_step_host with pinned host buffers -------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not heads:
         hq_ = [torch.empty((B, hq, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
         hk_ = [torch.empty((B, hkv, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
         hv_ = [torch.empty((B, hkv, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
@@ -326,9 +341,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             hv_[li].copy_(vs[li % R].cpu())
         e_steps = max(4, min(args.steps, 64))
 
-        def e2e_step():
+        streams2 = [stream, torch.cuda.Stream(device=dev)]
+
+        def e2e_step():  # layers alternate between two streams: copies overlap compute
             for li, ly in enumerate(layers):
-                ly.raas_decode_step_host(hq_[li], hk_[li], hv_[li], ho_[li], stream=stream)
+                ly.raas_decode_step_host(hq_[li], hk_[li], hv_[li], ho_[li], stream=streams2[li % 2])
 
         for _ in range(2):
             e2e_step()
@@ -337,9 +354,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             torch.distributed.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
+        torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(e_steps):
             e2e_step()
+        streams2[0].wait_stream(streams2[1])
         e1.record(stream)
         stream.synchronize()
         wall = time.perf_counter() - w0
@@ -351,7 +370,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                "unit": "decode steps/s", "steps": e_steps,
                "h2d_bytes_per_step": nl * (B * hq * d + 2 * B * hkv * d) * 2,
                "d2h_bytes_per_step": nl * B * hq * d * 2,
-               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out), one stream"}
+               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out), layers on 2 streams"}
 
     if rank != 0:
         return None
@@ -369,24 +388,29 @@ def run_ours(args, cfg, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if heads else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)",
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
                    "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
-                   "page": 16, "alpha": args.alpha, "parallelism": f"request-sharded x{world}, no collective",
+                   "page": 16, "alpha": args.alpha,
+                   "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
+                                   if heads else f"request-sharded x{world}, no collective"),
                    "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
                          "> 126 MB L2 (no flush needed)",
                    "steady_state": f"{fill_steps} decode steps before warmup (all pages used, evicting)"},
         "tokens_per_s": value * B,
+        "achieved_note": ("per-GPU HBM figures; the roofline covers this rank's decode launches"
+                          if world > 1 else None),
         "layer_steps_per_s": value * nl,
         "hbm_gbs": achieved,
         "pct_of_8tbs": achieved / 8000.0 * 100.0,
         "pct_of_measured_copy": achieved / peak * 100.0,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(cfg["workload"]),
-                     "kernel": "raas_decode_kernel<128,4,3>" if d == 128 else "raas_decode_kernel<64,4,3>",
+                     "kernel": f"raas_decode_kernel<{d},8,16> grid {info['grid']} x {info['block']} thr, "
+                               f"{info['smem']} B smem, {info['split_pages']}-page splits",
                      "algorithmic_bytes_per_launch": bytes_launch,
                      "avg_launch_us": launch_s * 1e6, "peak_source": peak_src,
                      "timing": "CUDA events on the launch stream around K graph replays of "
@@ -447,11 +471,21 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
+                    help="multi-GPU: shard requests (weak scaling) or kv-heads (strong, all-gather)")
+    ap.add_argument("--split-pages", type=int, default=0, help="override pages per split tile")
+    ap.add_argument("--dense", type=int, default=0,
+                    help="dense comparator: prefill N tokens, L > N + steps (no eviction)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.L:
         cfg["L"] = args.L
         cfg["workload"] += f"_L{args.L}"
+    if args.dense:  # dense decode comparator (P1): the whole context resident, nothing evicted
+        cfg["P"] = args.dense
+        cfg["L"] = ((args.dense + args.warmup + args.steps + 64) // 16 + 1) * 16
+        cfg["workload"] += f"_dense_N{args.dense}"
+        args.fill = 0
     if args.batch:
         cfg["batch"] = args.batch
     if args.layers:

@@ -6,10 +6,19 @@ import numpy as np, torch
 from paper_2502_11147_b200 import raas
 from paper_2502_11147_b200.raas import RaasLayer
 from paper_2502_11147_b200.synth import random_steady_state
-B, Hq, Hkv, d, P, L = 64, 32, 8, 128, 256, 2048
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("--B", type=int, default=64); ap.add_argument("--Hq", type=int, default=32)
+ap.add_argument("--Hkv", type=int, default=8); ap.add_argument("--L", type=int, default=2048)
+ap.add_argument("--P", type=int, default=256); ap.add_argument("--sp", type=int, default=0)
+ap.add_argument("--layers", type=int, default=8)
+a = ap.parse_args()
+B, Hq, Hkv, d, P, L = a.B, a.Hq, a.Hkv, 128, a.P, a.L
 C, Pp, U = L // 16, P // 16, B * Hkv
+Pp = -(-P // 16)
 meta = random_steady_state(77, U, C, Pp, Pp * 16 + 64 * (C - Pp) + 5)
-layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B) for _ in range(8)]
+layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=a.sp) for _ in range(a.layers)]
+print(layers[0].raas_launch_info())
 for ly in layers:
     ly.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"])
 q = torch.randn(B, Hq, d, device="cuda").bfloat16(); kv = torch.randn(B, Hkv, d, device="cuda").bfloat16()
@@ -33,7 +42,8 @@ b = buf[:g].astype(np.float64).sum(0) / g / (N * len(layers))
 names = {0: "prod tfree wait", 1: "prod empty wait (lane0)", 8: "prod total", 2: "merge mfull wait",
          7: "merge cq push wait", 9: "merge total", 4: "combine cq wait", 10: "combine total",
          5: "consumer full wait (sum 8 warps)", 6: "consumer q wait (sum)", 11: "consumer total (sum)"}
-print(f"launch {ms*1e3:.1f} us  ({537e6/(ms*1e-3)/1e9:.0f} GB/s)")
+nbytes = U * (4 * d * (L - 7.5) + 4 * d + 4 * (Hq // Hkv) * d + 12 * C)
+print(f"launch {ms*1e3:.1f} us  ({nbytes/(ms*1e-3)/1e9:.0f} GB/s)")
 for k, n in names.items():
     print(f"{n:34s} {b[k]:12.0f} cyc/launch/CTA")
 

@@ -4,6 +4,7 @@ Bar (BASELINE.json north_star): occupancy, timestamps and eviction order bit-exa
 differing stamp decision only where |p* - alpha| < 1e-6, counted (0 on this test set);
 attention output within max abs error 2e-2 (bf16 K/V, fp32 accumulation)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -349,3 +350,23 @@ def test_request_sharding_bitwise_at_full_size():
     assert np.array_equal(np.concatenate([lo, hi], axis=1), full)
     for k in ("ts", "start", "count", "t"):
         assert np.array_equal(np.concatenate([slo[k], shi[k]]), sf[k])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    """compute-sanitizer on a toy + multi-tile lockstep case (SURVEY §4 GPU self-tests)."""
+    import shutil
+    import subprocess
+    import sys
+
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("no compute-sanitizer")
+    script = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                          "sanitize_case.py")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable, script],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "sanitize case ok" in r.stdout
+    assert "ERROR SUMMARY: 0 errors" in r.stdout
