@@ -497,6 +497,10 @@ int raas_launch_info(const raas_handle* h, int32_t info[5]) {
 
 #ifdef RAAS_DBG_TIMING
 // tuning experiment only (not part of the ABI in include/raas.h): read + clear the cycle counters
+RAAS_API int raas_debug_units(uint64_t* out, int n) {
+  RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg_unit, sizeof(uint64_t) * n));
+  return RAAS_OK;
+}
 RAAS_API int raas_debug_timing(uint64_t* out, int n) {
   RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg, sizeof(uint64_t) * n));
   std::vector<uint64_t> z(1024 * 16, 0);

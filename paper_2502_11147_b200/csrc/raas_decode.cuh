@@ -29,6 +29,7 @@ namespace raas {
 
 #ifdef RAAS_DBG_TIMING  // tuning experiment: per-CTA cycle accounting of the pipeline waits
 __device__ unsigned long long g_raas_dbg[1024][16];
+__device__ unsigned long long g_raas_dbg_unit[4096][4];  // cta, pushed, combine start, end
 __device__ __forceinline__ long long dbg_clock() { return clock64(); }
 __device__ __forceinline__ void dbg_add(int slot, long long t0) {
   if ((threadIdx.x & 31) == 0) atomicAdd(&g_raas_dbg[blockIdx.x][slot], (unsigned long long)(clock64() - t0));
@@ -136,9 +137,15 @@ struct DecodeLayout {
   static constexpr int SCR = MAX_SPLITS * MAX_GROUP * 8 + 2 * MAX_GROUP * 4;
   static constexpr int OFF_SINFO = OFF_SCR + SCR;                          // int4[2] per stage
   static constexpr int OFF_TINFO = OFF_SINFO + S * 32;                     // int4[2] per parity
-  static constexpr int CQ = 8;                                             // combine queue
-  static constexpr int OFF_CQ = OFF_TINFO + 2 * 32;                         // int[CQ] unit ids
+  static constexpr int CQ = 16;                                            // combine queue
+  static constexpr int OFF_CQ = OFF_TINFO + 2 * 32;  // int[CQ] unit ids, then the pop counter
   static constexpr int OFF_BAR = OFF_CQ + CQ * 4 + 32;
+  // After its END sentinel a consumer's two ring stages (w, w+NC) are never written again, so
+  // for D = 128 it joins the combine pool with stage w as its scratch (the kernel's tail is
+  // the combines of the last units: more poppers, shorter tail).
+  static constexpr bool JOIN = STAGE >= SCR && S == 2 * NC;
+  static constexpr int NPOP = 1 + (JOIN ? NC : 0);
+  static_assert(CQ >= NPOP, "a popper may wait at most one queue phase ahead");
   // full[S], empty[S], qfull[2], mfull[2], tfree[2], cq_full[CQ], cq_empty[CQ]
   static constexpr int NBAR = 2 * S + 6 + 2 * CQ;
   static constexpr int BYTES = OFF_BAR + NBAR * 8;
@@ -173,22 +180,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
     if (ia < NE) { sts_f32(scr_w + 8 * ia, mla.x); sts_f32(scr_w + 8 * ia + 4, mla.y); }
     if (ib < NE) { sts_f32(scr_w + 8 * ib, mlb.x); sts_f32(scr_w + 8 * ib + 4, mlb.y); }
   }
-  __syncwarp();
-  if (lane < g) {  // LSE_h = M + log2 sum_s 2^(m_s - M) l_s   (log2 domain)
-    float M = -INFINITY;
-    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_w + 8 * (s * g + lane)));
-    float L = 0.f;
-    for (int s = 0; s < nse; ++s) {
-      const uint32_t a = scr_w + 8 * (s * g + lane);
-      const float w = fast_exp2(lds_f32(a) - M);
-      L += w * lds_f32(a + 4);
-      sts_f32(a, w);  // the split weight replaces m_s
-    }
-    sts_f32(scr_lse + 4 * lane, M + log2f(L));
-    sts_f32(scr_inv + 4 * lane, 1.f / L);
-  }
-  __syncwarp();
-  // ---- prefetch the first chunk of page metadata (used by a6/a7 below) ----
+  // page metadata for a6/a7, loaded while the split statistics are in flight
   constexpr int PPL = 4;  // pages per lane per chunk
   int tsv[PPL], stv[PPL];
   float pmv[PPL][MAX_GROUP];
@@ -206,49 +198,66 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
     }
   };
   load_meta(0);
+  __syncwarp();
+  if (lane < g) {  // LSE_h = M + log2 sum_s 2^(m_s - M) l_s   (log2 domain)
+    float M = -INFINITY;
+    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_w + 8 * (s * g + lane)));
+    float L = 0.f;
+    for (int s = 0; s < nse; ++s) {
+      const uint32_t a = scr_w + 8 * (s * g + lane);
+      const float w = fast_exp2(lds_f32(a) - M);
+      L += w * lds_f32(a + 4);
+      sts_f32(a, w);  // the split weight replaces m_s
+    }
+    sts_f32(scr_lse + 4 * lane, M + log2f(L));
+    sts_f32(scr_inv + 4 * lane, 1.f / L);
+  }
+  __syncwarp();
   // ---- a5 (2): out[h][d] = sum_s w_s acc_s[h][d] / L_h, float4 chunks ----
+  // blocks of 4 chunks per lane x 4 splits: 16 independent 16-byte loads in flight per lane
   constexpr int CPH = D / 4;                   // chunks per head
-  constexpr int CPL = MAX_GROUP * CPH / 32;    // chunks per lane (max)
-  constexpr int SG = 2;                        // splits per load group
+  constexpr int CB = 4, SG = 4;
   const int nch = g * CPH;
   const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
-  float4 o[CPL];
+  for (int cb = 0; 32 * cb < nch; cb += CB) {
+    float4 o[CB];
 #pragma unroll
-  for (int i = 0; i < CPL; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s0 = 0; s0 < nse; s0 += SG) {
-    float4 v[CPL][SG];
+    for (int i = 0; i < CB; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < nse; s0 += SG) {
+      float4 v[CB][SG];
 #pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      const int c = lane + 32 * i, h = c / CPH, d4 = c - h * CPH;
+      for (int i = 0; i < CB; ++i) {
+        const int c = lane + 32 * (cb + i), h = c / CPH, d4 = c - h * CPH;
 #pragma unroll
-      for (int u = 0; u < SG; ++u)
-        v[i][u] = (c < nch && s0 + u < nse)
-                      ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+        for (int u = 0; u < SG; ++u)
+          v[i][u] = (c < nch && s0 + u < nse)
+                        ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      const int c = lane + 32 * i, h = c / CPH;
-      if (c < nch) {
+      for (int i = 0; i < CB; ++i) {
+        const int c = lane + 32 * (cb + i), h = c / CPH;
+        if (c < nch) {
 #pragma unroll
-        for (int u = 0; u < SG; ++u) {
-          if (s0 + u < nse) {
-            const float w = lds_f32(scr_w + 8 * ((s0 + u) * g + h));
-            o[i].x += w * v[i][u].x; o[i].y += w * v[i][u].y;
-            o[i].z += w * v[i][u].z; o[i].w += w * v[i][u].w;
+          for (int u = 0; u < SG; ++u) {
+            if (s0 + u < nse) {
+              const float w = lds_f32(scr_w + 8 * ((s0 + u) * g + h));
+              o[i].x += w * v[i][u].x; o[i].y += w * v[i][u].y;
+              o[i].z += w * v[i][u].z; o[i].w += w * v[i][u].w;
+            }
           }
         }
       }
     }
-  }
 #pragma unroll
-  for (int i = 0; i < CPL; ++i) {
-    const int c = lane + 32 * i, h = c / CPH, d4 = c - h * CPH;
-    if (c < nch) {
-      const float inv = lds_f32(scr_inv + 4 * h);
-      const uint2 pk = make_uint2(pack_bf16x2(o[i].x * inv, o[i].y * inv),
-                                  pack_bf16x2(o[i].z * inv, o[i].w * inv));
-      *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) = pk;
+    for (int i = 0; i < CB; ++i) {
+      const int c = lane + 32 * (cb + i), h = c / CPH, d4 = c - h * CPH;
+      if (c < nch) {
+        const float inv = lds_f32(scr_inv + 4 * h);
+        const uint2 pk = make_uint2(pack_bf16x2(o[i].x * inv, o[i].y * inv),
+                                    pack_bf16x2(o[i].z * inv, o[i].w * inv));
+        *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) = pk;
+      }
     }
   }
   // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
@@ -314,6 +323,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
   int4* tinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_TINFO);
   volatile int* cq = reinterpret_cast<volatile int*>(smem_raw + (base - raw) + Lay::OFF_CQ);
   constexpr int CQ = Lay::CQ;
+  int* pop_ctr = reinterpret_cast<int*>(smem_raw + (base - raw) + Lay::OFF_CQ + CQ * 4);
   const uint32_t bar = base + Lay::OFF_BAR;
   auto full = [&](int s) { return bar + 8 * s; };
   auto empty = [&](int s) { return bar + 8 * (S + s); };
@@ -327,17 +337,18 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), 1);
+      mbar_init(empty(s), 32);  // every lane of the consuming warp releases its reads
     }
     for (int par = 0; par < 2; ++par) {
       mbar_init(qfull(par), 1);
-      mbar_init(mfull(par), NC);
-      mbar_init(tfree(par), 1);
+      mbar_init(mfull(par), NC * 32);  // every lane of every consumer arrives after its deposit
+      mbar_init(tfree(par), 32);       // every lane of the merge warp, after reading the deposits
     }
     for (int q = 0; q < CQ; ++q) {
       mbar_init(cqfull(q), 1);
       mbar_init(cqempty(q), 1);
     }
+    *pop_ctr = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -350,6 +361,32 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
 
   const int C = p.C, SP = p.split_pages, g = p.g;
   const int n_tiles = p.units * p.nsplit;
+
+  // multi-consumer combine queue: the combine warp from the start, the consumers after END
+  auto combine_loop = [&](uint32_t scratch) {
+    for (;;) {
+      int i = 0;
+      if (lane == 0) i = atomicAdd(pop_ctr, 1);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      const int q = i % CQ;
+      RAAS_TIMED(4, mbar_wait(cqfull(q), (i / CQ) & 1));
+      int entry = 0;
+      if (lane == 0) entry = cq[q];
+      entry = __shfl_sync(0xffffffffu, entry, 0);
+      if (lane == 0) mbar_arrive(cqempty(q));  // the entry is read: the slot may be refilled
+      if (entry < 0) break;
+      const int unit = entry & (CQ_OWNED - 1);
+      if (!(entry & CQ_OWNED)) fence_acq_rel_gpu();  // partials from other SMs (acquired by merge)
+#ifdef RAAS_DBG_TIMING
+      if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
+#endif
+      combine_unit<D>(p, unit, scratch, lane);
+#ifdef RAAS_DBG_TIMING
+      if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
+#endif
+      __syncwarp();
+    }
+  };
 
   if (warp == 0) {
     // =============================== TMA producer ===============================
@@ -398,7 +435,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         tinfo[2 * par + 1] = make_int4((int)j, 0, owned ? 1 : 0, 0);
         mbar_arrive_expect_tx(qfull(par), g * D * 2);
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
-        if (n < NC) mbar_arrive_cnt(mfull(par), NC - n);  // warps with no page in this tile
+        if (n < NC) mbar_arrive_cnt(mfull(par), (NC - n) * 32);  // warps with no page here
       }
       // pages in batches, one lane per page: each lane waits for its stage, fills the stage
       // info and issues one 1-D bulk copy of the page (K rows then V rows, 16*D*4 contiguous
@@ -440,7 +477,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1);
     if (lane == 0) {
       tinfo[2 * par + 1] = make_int4(0, FLAG_END, 0, 0);
-      mbar_arrive_cnt(mfull(par), NC);
+      mbar_arrive_cnt(mfull(par), NC * 32);
     }
     dbg_add(8, t_start);
 #ifdef RAAS_DBG_TIMING
@@ -451,6 +488,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     const int r = lane >> 2, qd = lane & 3;
     int npush = 0;
     auto push = [&](int unit) {  // hand a finished unit (or -1 = END) to the combine warp
+#ifdef RAAS_DBG_TIMING
+      if (lane == 0 && unit >= 0 && (unit & (CQ_OWNED - 1)) < 4096) g_raas_dbg_unit[unit & (CQ_OWNED - 1)][1] = dbg_gtimer();
+#endif
       const int q = npush % CQ;
       RAAS_TIMED(7, mbar_wait(cqempty(q), ((npush / CQ) & 1) ^ 1));
       if (lane == 0) {
@@ -465,7 +505,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       RAAS_TIMED(2, mbar_wait(mfull(par), (k >> 1) & 1));
       const int4 t0 = tinfo[2 * par], t1 = tinfo[2 * par + 1];
       if (t1.y & FLAG_END) {
-        push(-1);
+        for (int e = 0; e < Lay::NPOP; ++e) push(-1);
         break;
       }
       const int unit = t0.x, split = t0.y, nse = t0.z, n = t0.w, J = t1.x, owned = t1.z;
@@ -494,7 +534,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(tfree(par));  // deposits / q / info of tile k consumed
+      mbar_arrive(tfree(par));  // deposits / q / info of tile k consumed (each lane's reads)
       // publish the tile's split-K partial (m, l, acc) in the C-fragment layout
       const int pbase = (unit * p.nsplit + split) * g;
       if (lane < 4) {
@@ -521,17 +561,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     dbg_add(9, t_start);
   } else if (warp == 2) {
     // ============================ combine (per unit) ============================
-    for (int i = 0;; ++i) {
-      const int q = i % CQ;
-      RAAS_TIMED(4, mbar_wait(cqfull(q), (i / CQ) & 1));
-      const int entry = cq[q];
-      if (entry < 0) break;
-      const int unit = entry & (CQ_OWNED - 1);
-      if (!(entry & CQ_OWNED)) fence_acq_rel_gpu();  // partials from other SMs (acquired by merge)
-      combine_unit<D>(p, unit, scr, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(cqempty(q));
-    }
+    combine_loop(scr);
     dbg_add(10, t_start);
 #ifdef RAAS_DBG_TIMING
     if (lane == 0) g_raas_dbg[blockIdx.x][14] = dbg_gtimer();
@@ -554,10 +584,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       RAAS_TIMED(5, mbar_wait(full(s), (j / S) & 1));
       const int4 i0 = sinfo[2 * s], i1 = sinfo[2 * s + 1];
       const int flags = i1.y;
-      if (flags & FLAG_END) break;
+      if (flags & FLAG_END) {
+        if constexpr (Lay::JOIN) combine_loop(ring + w * STAGE);  // join the tail's combines
+        break;
+      }
       if (flags & FLAG_SKIP) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty(s));
+        mbar_arrive(empty(s));
         continue;
       }
       const int unit = i0.x, page = i0.y, cnt = i0.z, patch = i0.w, k = i1.x, par = k & 1;
@@ -598,10 +631,10 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
 
 #ifdef RAAS_DBG_NOCOMPUTE  // pipeline-ceiling experiment: consume without computing
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty(s));
+      mbar_arrive(empty(s));
       if (flags & FLAG_LAST) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(mfull(par));
+        mbar_arrive(mfull(par));  // each lane releases its own deposit writes
       }
       continue;
 #endif
@@ -662,7 +695,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty(s));  // stage free for the producer
+      mbar_arrive(empty(s));  // stage free for the producer
 
       if (flags & FLAG_LAST) {  // deposit this warp's softmax state for the tile merge
 #pragma unroll
@@ -680,7 +713,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         sts_f32(dep + 128 * (KS * 4 + 2), l0);
         sts_f32(dep + 128 * (KS * 4 + 3), l1);
         __syncwarp();
-        if (lane == 0) mbar_arrive(mfull(par));
+        mbar_arrive(mfull(par));  // each lane releases its own deposit writes
       }
     }
     dbg_add(11, t_start);
