@@ -36,7 +36,7 @@ CONFIGS = {
     1: dict(workload="toy_4q2kv_d64_L64", model="toy", hq=4, hkv=2, d=64, layers=1, batch=1,
             P=32, L=64, decode=256),
     2: dict(workload="llama31_8b_b1_L1024", model="Llama-3.1-8B attention (32q/8kv, d=128)",
-            hq=32, hkv=8, d=128, layers=32, batch=1, P=512, L=1024, decode=8192, split_pages=2),
+            hq=32, hkv=8, d=128, layers=32, batch=1, P=512, L=1024, decode=8192, split_pages=16),
     3: dict(workload="llama31_8b_b64_L2048", model="Llama-3.1-8B attention (32q/8kv, d=128)",
             hq=32, hkv=8, d=128, layers=32, batch=64, P=256, L=2048, decode=16384),
     4: dict(workload="r1_distill_qwen7b_b32pergpu_L4096",

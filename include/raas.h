@@ -69,7 +69,7 @@ typedef struct {
   int32_t head_dim;      /* 64 or 128 */
   int32_t batch;         /* requests held by this handle */
   float   softmax_scale; /* 0 => 1/sqrt(head_dim) */
-  int32_t split_pages;   /* pages per split-K tile; 0 => auto (8, raised so L/16/split <= 128).
+  int32_t split_pages;   /* pages per split-K tile; 0 => auto (min(32, L/16), raised so L/16/split <= 80).
                             Independent of batch, so results are bitwise identical under
                             request sharding. */
 } raas_config;

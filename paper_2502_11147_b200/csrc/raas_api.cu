@@ -78,8 +78,8 @@ int derive(const raas_config* c, Derived* d) {
   d->units = c->batch * c->n_kv_heads;
   if ((long long)d->units * d->C * raas::PAGE >= (1LL << 31))
     return fail(RAAS_E_UNSUPPORTED, "units * L too large for 32-bit TMA row coordinates");
-  // auto: a quarter of the budget per split, 4..32 pages (depends on L only, never on batch)
-  int sp = c->split_pages > 0 ? c->split_pages : std::max(4, std::min(32, d->C / 4));
+  // auto: 32-page splits (the whole budget when L <= 512); depends on L only, never on batch
+  int sp = c->split_pages > 0 ? c->split_pages : std::min(32, d->C);
   if (sp > 32) return fail(RAAS_E_UNSUPPORTED, "split_pages must be <= 32");
   const int min_sp = (d->C + raas::MAX_SPLITS - 1) / raas::MAX_SPLITS;
   if (sp < min_sp) sp = min_sp;
@@ -220,6 +220,31 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   return RAAS_OK;
 }
 
+// Grid size for the unit-affine schedule (raas_decode.cuh TileSched): minimise the estimated
+// critical path = the largest tile count of a CTA, plus, when some units are shared across CTAs,
+// the cross-CTA combine that ends the kernel (~8 us, expressed in tiles of SP pages streamed at
+// ~48 GB/s per SM: 8 KiB per page).  The result never changes numerics (the split arithmetic is
+// schedule-free), only the speed.
+int choose_grid(int units, int nsplit, int sp, int cap) {
+  const long long tiles = (long long)units * nsplit;
+  if (tiles <= 0) return 1;
+  const double tile_us = sp * 8192.0 / 48e3;  // us per tile
+  const double tail_tiles = 8.0 / tile_us;
+  int best = 1;
+  double best_cost = 1e30;
+  const int hi = (int)std::min<long long>(cap, tiles);
+  for (int G = 1; G <= hi; ++G) {
+    const int fu = units / G, R = units - fu * G;
+    const long long shared = (long long)R * nsplit;
+    const double cost = (double)fu * nsplit + (double)((shared + G - 1) / G) + (R > 0 ? tail_tiles : 0.0);
+    if (cost < best_cost - 1e-9 || (cost < best_cost + 1e-9 && G > best)) {
+      best_cost = cost;
+      best = G;
+    }
+  }
+  return best;
+}
+
 template <int D>
 int setup_kernel(raas_handle* h) {
   auto k = decode_kernel<D>();
@@ -228,9 +253,7 @@ int setup_kernel(raas_handle* h) {
   int per_sm = 0;
   RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
-  const long long need = (long long)h->d.units * h->d.nsplit;  // one tile per CTA at most
-  const long long cap = (long long)h->num_sms * per_sm;
-  h->grid = (int)(need < cap ? need : cap);
+  h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
   return RAAS_OK;
 }
 
