@@ -341,11 +341,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             hv_[li].copy_(vs[li % R].cpu())
         e_steps = max(4, min(args.steps, 64))
 
-        streams2 = [stream, torch.cuda.Stream(device=dev)]
-
-        def e2e_step():  # layers alternate between two streams: copies overlap compute
+        def e2e_step():  # one stream: H2D, step, D2H of every layer in order (no overlap)
             for li, ly in enumerate(layers):
-                ly.raas_decode_step_host(hq_[li], hk_[li], hv_[li], ho_[li], stream=streams2[li % 2])
+                ly.raas_decode_step_host(hq_[li], hk_[li], hv_[li], ho_[li], stream=stream)
 
         for _ in range(2):
             e2e_step()
@@ -358,7 +356,6 @@ def run_ours(args, cfg, rank, world, local_rank):
         e0.record(stream)
         for _ in range(e_steps):
             e2e_step()
-        streams2[0].wait_stream(streams2[1])
         e1.record(stream)
         stream.synchronize()
         wall = time.perf_counter() - w0
@@ -370,7 +367,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                "unit": "decode steps/s", "steps": e_steps,
                "h2d_bytes_per_step": nl * (B * hq * d + 2 * B * hkv * d) * 2,
                "d2h_bytes_per_step": nl * B * hq * d * 2,
-               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out), layers on 2 streams"}
+               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out), one stream, layers in order"}
 
     if rank != 0:
         return None

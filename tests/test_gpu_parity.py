@@ -243,11 +243,17 @@ def test_error_codes_gpu():
 # ------------------------------------------------------------------ full-size sampled parity
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,L,P", [(64, 32, 8, 2048, 256), (32, 28, 4, 4096, 128)])
-def test_full_size_sampled_units_lockstep(oracle_mod, B, Hq, Hkv, L, P):
-    """BASELINE.json configs[2] / [3] shapes in the launch configuration bench.py times:
-    the whole batch runs on the GPU from a full-cache state; the first and last request
-    (all kv-heads) are replayed on the oracle in lockstep with resync."""
+@pytest.mark.parametrize("B,Hq,Hkv,L,P,sp", [
+    (64, 32, 8, 2048, 256, 0),   # config 3 (headline)
+    (32, 28, 4, 4096, 128, 0),   # config 4 (per GPU)
+    (1, 32, 8, 1024, 512, 16),   # config 2 (B = 1, 16-page splits as benched)
+    (8, 32, 8, 8192, 128, 0),    # config 5, largest budget (16 splits per unit)
+    (16, 32, 8, 256, 128, 0),    # config 5, smallest budget (one split per unit)
+])
+def test_full_size_sampled_units_lockstep(oracle_mod, B, Hq, Hkv, L, P, sp):
+    """BASELINE.json configs' shapes in the launch configuration bench.py times: the whole
+    batch runs on the GPU from a full-cache state; the first and last request (all kv-heads)
+    are replayed on the oracle in lockstep with resync."""
     d, T = 128, 24
     C, Pp = L // PAGE, -(-P // PAGE)
     U = B * Hkv
@@ -256,9 +262,9 @@ def test_full_size_sampled_units_lockstep(oracle_mod, B, Hq, Hkv, L, P):
     rng = np.random.Generator(np.random.Philox(78))
     kst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
     vst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
-    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=sp)
     layer.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"], kst, vst)
-    sample = [0, B - 1]
+    sample = sorted({0, B - 1})
     units = [b * Hkv + h for b in sample for h in range(Hkv)]
     orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
                             batch=len(sample))
