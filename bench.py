@@ -225,7 +225,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 * args.config + rank)
     sp = args.split_pages if args.split_pages else cfg.get("split_pages", 0)
-    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp) for _ in range(nl)]
+    score_mode = 1 if args.score == "quest" else 0
+    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode)
+              for _ in range(nl)]
     info = layers[0].raas_launch_info()
     for ly in layers:
         k = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
@@ -391,7 +393,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)",
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
                    "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
-                   "page": 16, "alpha": args.alpha,
+                   "page": 16, "alpha": args.alpha, "score_mode": args.score,
                    "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
                                    if heads else f"request-sharded x{world}, no collective"),
                    "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
@@ -471,6 +473,8 @@ def main():
     ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
                     help="multi-GPU: shard requests (weak scaling) or kv-heads (strong, all-gather)")
     ap.add_argument("--split-pages", type=int, default=0, help="override pages per split tile")
+    ap.add_argument("--score", default="exact", choices=["exact", "quest"],
+                    help="page score for stamping: exact page max (D4) or Quest bound (NEXT-1)")
     ap.add_argument("--dense", type=int, default=0,
                     help="dense comparator: prefill N tokens, L > N + steps (no eviction)")
     args = ap.parse_args()

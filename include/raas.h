@@ -72,6 +72,12 @@ typedef struct {
   int32_t split_pages;   /* pages per split-K tile; 0 => auto (min(32, L/16), raised so L/16/split <= 80).
                             Independent of batch, so results are bitwise identical under
                             request sharding. */
+  int32_t score_mode;    /* page score the stamp compares with alpha:
+                            0 = exact page max of the normalised scores (reading D4, default);
+                            1 = Quest representative-key bound, the paper's estimator (§3.3
+                                :147-151, App. B :362): per channel c, max(q_c min_c, q_c max_c)
+                                over the page's keys, summed, scaled and normalised by the step's
+                                LSE (reading D22).  A superset of mode 0's stamps. */
 } raas_config;
 
 /* Bytes of device memory the handle needs (KV store: per unit L/16 pages, each 16 K rows + 16 V

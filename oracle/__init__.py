@@ -47,6 +47,7 @@ class _Cfg(ctypes.Structure):
         ("head_dim", ctypes.c_int32),
         ("batch", ctypes.c_int32),
         ("softmax_scale", ctypes.c_double),
+        ("score_mode", ctypes.c_int32),
     ]
 
 
@@ -91,8 +92,9 @@ class Oracle:
     """fp64 RaaS state machine over `batch * n_kv_heads` independent units (host)."""
 
     def __init__(self, L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch,
-                 softmax_scale=0.0):
-        self.cfg = _Cfg(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale)
+                 softmax_scale=0.0, score_mode=0):
+        self.cfg = _Cfg(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
+                        score_mode)
         self.C = L // page if page > 0 else 0
         self.units = batch * n_kv_heads
         self.page, self.d, self.hq, self.hkv, self.batch = page, head_dim, n_q_heads, n_kv_heads, batch

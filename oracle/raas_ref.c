@@ -74,6 +74,7 @@ int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
     return REF_E_INVALID;
   if (cfg->head_dim <= 0 || cfg->batch <= 0) return REF_E_INVALID;
   if (!(cfg->alpha >= 0.0)) return REF_E_INVALID;
+  if (cfg->score_mode != 0 && cfg->score_mode != 1) return REF_E_INVALID;
   raas_ref* h = (raas_ref*)calloc(1, sizeof *h);
   if (!h) return REF_E_INVALID;
   h->cfg = *cfg;
@@ -228,13 +229,33 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
           for (int32_t c = 0; c < d; ++c) o[c] += w * vj[c];
         }
     }
-    /* decisive log-probability per page: max over heads of the group and tokens (D4, D5) */
+    /* decisive log-score per page, max over the heads of the group (D5):
+     *  mode 0: exact page max of the normalised scores (D4);
+     *  mode 1: Quest's bound -- "a representative key (K) for each page ... the query (Q) ...
+     *          attends to these representative keys to compute a single attention score per
+     *          page" (:147-151, :362): per channel c, max(q_c * min_j k_jc, q_c * max_j k_jc)
+     *          summed over c, scaled, normalised by the step's LSE (D22). */
     for (int32_t p = 0; p < C; ++p) {
-      if (u->pinned[p]) continue;
-      for (int32_t i = 0; i < u->count[p]; ++i) {
-        const double lp = s[p * page + i] - lse;
-        if (lp > best[p]) best[p] = lp;
+      if (u->pinned[p] || u->count[p] == 0) continue;
+      double lp = -INFINITY;
+      if (h->cfg.score_mode == 0) {
+        for (int32_t i = 0; i < u->count[p]; ++i)
+          if (s[p * page + i] - lse > lp) lp = s[p * page + i] - lse;
+      } else {
+        double U = 0.0;
+        for (int32_t c = 0; c < d; ++c) {
+          double mn = INFINITY, mx = -INFINITY;
+          for (int32_t i = 0; i < u->count[p]; ++i) {
+            const double kc = u->K[((size_t)p * page + i) * d + c];
+            if (kc < mn) mn = kc;
+            if (kc > mx) mx = kc;
+          }
+          const double a = qh[c] * mn, b = qh[c] * mx;
+          U += a > b ? a : b;
+        }
+        lp = h->scale * U - lse;
       }
+      if (lp > best[p]) best[p] = lp;
     }
   }
   /* stamp: "we assign it the latest timestamp" when the score is above alpha (:29, :98,

@@ -37,6 +37,12 @@ typedef struct {
   int32_t head_dim;
   int32_t batch;
   double  softmax_scale; /* 0 => 1/sqrt(head_dim) */
+  int32_t score_mode;    /* page score used for stamping:
+                            0 = exact page max of the normalised scores (reading D4);
+                            1 = Quest representative-key bound (§3.3 :147-151, App. B
+                                :362): U_p = sum_c max(q_c min_c, q_c max_c) over the per-channel
+                                min / max of the page's keys, estimated score exp(scale U_p - LSE)
+                                (reading D22; "parity unpinned": the paper gives no formula) */
 } raas_ref_config;
 
 typedef struct raas_ref raas_ref;

@@ -69,6 +69,7 @@ int derive(const raas_config* c, Derived* d) {
   if (c->n_q_heads % c->n_kv_heads != 0) return fail(RAAS_E_INVALID, "n_q_heads %% n_kv_heads != 0");
   if (!(c->alpha >= 0.f)) return fail(RAAS_E_INVALID, "alpha must be >= 0");
   if (c->softmax_scale < 0.f) return fail(RAAS_E_INVALID, "softmax_scale must be >= 0");
+  if (c->score_mode != 0 && c->score_mode != 1) return fail(RAAS_E_INVALID, "score_mode must be 0 or 1");
   if (c->page != raas::PAGE) return fail(RAAS_E_UNSUPPORTED, "page must be 16");
   if (c->head_dim != 64 && c->head_dim != 128)
     return fail(RAAS_E_UNSUPPORTED, "head_dim must be 64 or 128");
@@ -201,6 +202,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.nsplit = h->d.nsplit;
   p.split_pages = h->d.split_pages;
   p.g = h->d.g;
+  p.score_mode = h->cfg.score_mode;
   const float scale = h->cfg.softmax_scale > 0.f ? h->cfg.softmax_scale
                                                  : 1.0f / sqrtf((float)h->cfg.head_dim);
   p.scale_log2 = scale * 1.4426950408889634f;

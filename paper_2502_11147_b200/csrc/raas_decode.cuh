@@ -661,10 +661,58 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         pm0 = fmaxf(pm0, __shfl_xor_sync(0xffffffffu, pm0, o));
         pm1 = fmaxf(pm1, __shfl_xor_sync(0xffffffffu, pm1, o));
       }
-      if (lane < 4) {  // a4: page-max logit per head ("a single attention score per page", :147)
+      float sc0 = pm0, sc1 = pm1;  // the page score the stamp will use (log2 domain)
+      if (p.score_mode == 1) {
+        // Quest's representative-key bound (PAPER.md :147-151, :362; reading D22): per channel
+        // c, max(q_c min_c, q_c max_c) over the page's valid keys, summed over c.  Lane l owns
+        // channels [l*CQ, (l+1)*CQ); the page is already in shared memory (no extra HBM bytes).
+        constexpr int CQL = D / 32;
+        const int c0 = lane * CQL, chk = c0 >> 3, wi = c0 & 7;
+        float mnv[CQL], mxv[CQL];
+#pragma unroll
+        for (int i = 0; i < CQL; ++i) { mnv[i] = INFINITY; mxv[i] = -INFINITY; }
+        for (int row = 0; row < cnt; ++row) {
+          const uint32_t a = kb + row * ROW + ((chk ^ (row & 7)) << 4) + wi * 2;
+          uint32_t w[CQL / 2];
+          if constexpr (CQL == 4) {
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(a));
+          } else {
+            w[0] = lds_u32(a);
+          }
+#pragma unroll
+          for (int i = 0; i < CQL; ++i) {
+            const float kv = __uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16));
+            mnv[i] = fminf(mnv[i], kv);
+            mxv[i] = fmaxf(mxv[i], kv);
+          }
+        }
+        const uint32_t qh0 = qbuf + par * Lay::QBUF + c0 * 2;
+        sc0 = sc1 = -INFINITY;
+#pragma unroll
+        for (int h = 0; h < MAX_GROUP; ++h) {
+          if (h < g) {
+            uint32_t w[CQL / 2];
+            if constexpr (CQL == 4) {
+              asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(qh0 + h * D * 2));
+            } else {
+              w[0] = lds_u32(qh0 + h * D * 2);
+            }
+            float part = 0.f;
+#pragma unroll
+            for (int i = 0; i < CQL; ++i) {
+              const float qv = __uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16));
+              part += fmaxf(qv * mnv[i], qv * mxv[i]);
+            }
+            const float U = warp_sum(part) * p.scale_log2;
+            if (h == 2 * qd) sc0 = U;
+            if (h == 2 * qd + 1) sc1 = U;
+          }
+        }
+      }
+      if (lane < 4) {  // a4: page score per head ("a single attention score per page", :147)
         float* pmx = p.pmax + (size_t)(unit * C + page) * g;
-        if (2 * qd < g) pmx[2 * qd] = pm0;
-        if (2 * qd + 1 < g) pmx[2 * qd + 1] = pm1;
+        if (2 * qd < g) pmx[2 * qd] = sc0;
+        if (2 * qd + 1 < g) pmx[2 * qd + 1] = sc1;
       }
       const float mn0 = fmaxf(m0, pm0), mn1 = fmaxf(m1, pm1);
       const float cr0 = fast_exp2(m0 - mn0), cr1 = fast_exp2(m1 - mn1);

@@ -45,6 +45,7 @@ struct DecodeParams {
   uint32_t* status;
   unsigned long long* stats;  // [4]: stamps, decisions, evictions, unit-steps
   int units, C, nsplit, split_pages, g;
+  int score_mode;    // 0 exact page max (D4), 1 Quest representative-key bound (D22)
   float scale_log2;  // softmax_scale * log2(e)
   float log2_alpha;  // log2(alpha); -inf for alpha == 0
 };

@@ -34,6 +34,7 @@ class raas_config(ctypes.Structure):
         ("batch", ctypes.c_int32),
         ("softmax_scale", ctypes.c_float),
         ("split_pages", ctypes.c_int32),
+        ("score_mode", ctypes.c_int32),
     ]
 
 
@@ -92,10 +93,13 @@ def _check(rc, what):
         raise RaasError(rc, what)
 
 
+SCORE_EXACT, SCORE_QUEST = 0, 1
+
+
 def make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch, page=16, softmax_scale=0.0,
-                split_pages=0) -> raas_config:
+                split_pages=0, score_mode=SCORE_EXACT) -> raas_config:
     return raas_config(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
-                       split_pages)
+                       split_pages, score_mode)
 
 
 def raas_arena_bytes(cfg: raas_config) -> int:
@@ -126,11 +130,12 @@ class RaasLayer:
     """One libraas handle (one attention layer of `batch` requests) plus its device arena."""
 
     def __init__(self, L, alpha, n_q_heads, n_kv_heads, head_dim, batch, device=None,
-                 softmax_scale=0.0, split_pages=0):
+                 softmax_scale=0.0, split_pages=0, score_mode=SCORE_EXACT):
         import torch
 
         self.cfg = make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch,
-                               softmax_scale=softmax_scale, split_pages=split_pages)
+                               softmax_scale=softmax_scale, split_pages=split_pages,
+                               score_mode=score_mode)
         self.device = torch.device(device if device is not None else "cuda")
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         nbytes = raas_arena_bytes(self.cfg)

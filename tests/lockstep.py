@@ -54,15 +54,16 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True):
 
 
 def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_every=1,
-                 layer=None, oracle=None, device="cuda", on_step=None):
+                 layer=None, oracle=None, device="cuda", on_step=None, score_mode=0):
     """Drive both sides through the whole stream; returns LockstepResult."""
     B, _, P, d = stream.k_pre.shape
     if layer is None:
-        layer = RaasLayer(L, alpha, Hq, Hkv, d, B, device=device, split_pages=split_pages)
+        layer = RaasLayer(L, alpha, Hq, Hkv, d, B, device=device, split_pages=split_pages,
+                          score_mode=score_mode)
         layer.raas_prefill(to_dev(stream.k_pre, device), to_dev(stream.v_pre, device), P)
     if oracle is None:
         oracle = oracle_mod.Oracle(L=L, alpha=alpha, page=16, n_q_heads=Hq, n_kv_heads=Hkv,
-                                   head_dim=d, batch=B)
+                                   head_dim=d, batch=B, score_mode=score_mode)
         oracle.prefill(stream.k_pre, stream.v_pre, P)
     res = LockstepResult()
     out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=device)

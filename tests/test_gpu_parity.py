@@ -376,3 +376,42 @@ def test_compute_sanitizer(tool):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "sanitize case ok" in r.stdout
     assert "ERROR SUMMARY: 0 errors" in r.stdout or "(0 errors, 0 warnings)" in r.stdout
+
+
+# ------------------------------------------------------------------ NEXT-1: Quest bound mode
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,lam", [
+    (2, 8, 2, 128, 40, 300, 256, 0, 6.0),
+    (2, 28, 4, 128, 64, 200, 512, 8, 6.0),
+    (1, 4, 2, 64, 32, 256, 64, 0, 6.0),       # toy shapes
+    (2, 16, 2, 128, 20, 220, 160, 3, 8.0),
+])
+def test_quest_mode_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, lam):
+    """score_mode = 1 (Quest representative-key bound, PAPER.md :147-151, :362) against the
+    oracle's Quest mode: bit-exact state, 0 band events, out within 2e-2."""
+    st = waterfall_stream(300 + B + Hq + P, B, Hq, Hkv, d, P, T, lam=lam)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, split_pages=sp,
+                                 score_mode=1)
+    assert res.band_events == 0
+    assert res.max_err <= OUT_TOL
+    assert res.evictions > 0
+
+
+def test_quest_stamps_superset_of_exact_on_gpu():
+    """Same inputs, no eviction (L >= N): every page the exact mode stamps, Quest stamps too."""
+    B, Hq, Hkv, d, P, T, L = 2, 8, 2, 128, 40, 80, 256
+    st = waterfall_stream(41, B, Hq, Hkv, d, P, T)
+    states = []
+    for mode in (0, 1):
+        layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B, score_mode=mode)
+        layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+        out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
+        per = []
+        for i in range(T):
+            layer.raas_decode_step(to_dev(st.q[i]), to_dev(st.k[i]), to_dev(st.v[i]), out)
+            per.append(layer.raas_get_state()["ts"].copy())
+        states.append(np.stack(per))
+    t_now = (P + 1 + np.arange(T))[:, None, None]
+    ex, qu = states[0] == t_now, states[1] == t_now
+    assert (qu | ~ex).all() and (qu & ~ex).any()

@@ -440,3 +440,51 @@ def test_d3_strict_threshold(oracle_mod):
     st = o.get_state()
     ts = {int(s): int(t) for s, t, c in zip(st["start"][0], st["ts"][0], st["count"][0]) if c}
     assert ts == {1: 0, 2: 4, 3: 4, 4: 4}
+
+
+# ---------------------------------------------------------------- NEXT-1: Quest bound mode
+
+
+def _dense_pstars(oracle_mod, st, g, score_mode, page=PAGE):
+    B, Hkv, P, d = st.k_pre.shape
+    L = ((P + st.T) // page + 2) * page
+    o = oracle_mod.Oracle(L=L, alpha=1e-4, page=page, n_q_heads=g * Hkv, n_kv_heads=Hkv,
+                          head_dim=d, batch=B, score_mode=score_mode)
+    o.prefill(st.k_pre, st.v_pre, P)
+    out = []
+    for i in range(st.T):
+        o.decode_step(st.q[i], st.k[i], st.v[i])
+        out.append(o.get_trace()["pstar"].copy())
+    return np.stack(out)
+
+
+def test_quest_bound_dominates_exact_page_max(oracle_mod):
+    """Quest's per-channel min/max bound (PAPER.md :147-151, :362) is an upper bound of every
+    token's logit in the page, so with identical residency (L >= N: no eviction) its estimated
+    score is >= the exact page max everywhere, and its stamp set is a superset."""
+    st = waterfall_stream(17, 2, 8, 2, 64, 40, 60)
+    ex = _dense_pstars(oracle_mod, st, 4, 0)
+    qu = _dense_pstars(oracle_mod, st, 4, 1)
+    valid = ex >= 0
+    assert valid.any()
+    assert (qu[valid] >= ex[valid] * (1 - 1e-12)).all()
+    assert ((qu > 1e-4) | ~(ex > 1e-4)).all()          # stamps(quest) ⊇ stamps(exact)
+    assert (qu[valid] > ex[valid] * (1 + 1e-9)).any()  # and strictly looser somewhere
+
+
+def test_quest_bound_is_exact_for_single_token_pages(oracle_mod):
+    """page = 1: the representative key IS the key, so both modes give the same scores."""
+    st = gaussian_stream(18, 2, 4, 2, 16, 5, 30)
+    ex = _dense_pstars(oracle_mod, st, 2, 0, page=1)
+    qu = _dense_pstars(oracle_mod, st, 2, 1, page=1)
+    assert np.allclose(qu, ex, rtol=1e-12, atol=0)
+
+
+def test_quest_bound_is_exact_for_identical_keys(oracle_mod):
+    """All keys of a page equal: min = max = k, so U = q.k exactly (P3' page twin data)."""
+    g_, st = page_twin_stream(g_heads=2, value_seed=1)
+    st.T  # noqa: B018
+    short = type(st)(st.k_pre, st.v_pre, st.q[:40], st.k[:40], st.v[:40])
+    ex = _dense_pstars(oracle_mod, short, 2, 0)
+    qu = _dense_pstars(oracle_mod, short, 2, 1)
+    assert np.allclose(qu, ex, rtol=1e-12, atol=0)
