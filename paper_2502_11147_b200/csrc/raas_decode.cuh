@@ -668,9 +668,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         // channels [l*CQ, (l+1)*CQ); the page is already in shared memory (no extra HBM bytes).
         constexpr int CQL = D / 32;
         const int c0 = lane * CQL, chk = c0 >> 3, wi = c0 & 7;
-        float mnv[CQL], mxv[CQL];
+        uint32_t mnp[CQL / 2], mxp[CQL / 2];  // packed bf16x2 running min / max (exact)
 #pragma unroll
-        for (int i = 0; i < CQL; ++i) { mnv[i] = INFINITY; mxv[i] = -INFINITY; }
+        for (int i = 0; i < CQL / 2; ++i) { mnp[i] = 0x7f807f80u; mxp[i] = 0xff80ff80u; }
         for (int row = 0; row < cnt; ++row) {
           const uint32_t a = kb + row * ROW + ((chk ^ (row & 7)) << 4) + wi * 2;
           uint32_t w[CQL / 2];
@@ -680,11 +680,16 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
             w[0] = lds_u32(a);
           }
 #pragma unroll
-          for (int i = 0; i < CQL; ++i) {
-            const float kv = __uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16));
-            mnv[i] = fminf(mnv[i], kv);
-            mxv[i] = fmaxf(mxv[i], kv);
+          for (int i = 0; i < CQL / 2; ++i) {
+            asm("min.bf16x2 %0, %0, %1;" : "+r"(mnp[i]) : "r"(w[i]));
+            asm("max.bf16x2 %0, %0, %1;" : "+r"(mxp[i]) : "r"(w[i]));
           }
+        }
+        float mnv[CQL], mxv[CQL];
+#pragma unroll
+        for (int i = 0; i < CQL; ++i) {
+          mnv[i] = __uint_as_float((i & 1) ? (mnp[i >> 1] & 0xffff0000u) : (mnp[i >> 1] << 16));
+          mxv[i] = __uint_as_float((i & 1) ? (mxp[i >> 1] & 0xffff0000u) : (mxp[i >> 1] << 16));
         }
         const uint32_t qh0 = qbuf + par * Lay::QBUF + c0 * 2;
         sc0 = sc1 = -INFINITY;

@@ -383,7 +383,7 @@ def test_compute_sanitizer(tool):
 
 @pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,lam", [
     (2, 8, 2, 128, 40, 300, 256, 0, 6.0),
-    (2, 28, 4, 128, 64, 200, 512, 8, 6.0),
+    (2, 28, 4, 128, 64, 200, 192, 4, 6.0),
     (1, 4, 2, 64, 32, 256, 64, 0, 6.0),       # toy shapes
     (2, 16, 2, 128, 20, 220, 160, 3, 8.0),
 ])
