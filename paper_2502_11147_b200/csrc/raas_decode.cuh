@@ -692,9 +692,10 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           mxv[i] = __uint_as_float((i & 1) ? (mxp[i >> 1] & 0xffff0000u) : (mxp[i >> 1] << 16));
         }
         const uint32_t qh0 = qbuf + par * Lay::QBUF + c0 * 2;
-        sc0 = sc1 = -INFINITY;
+        float v[MAX_GROUP];
 #pragma unroll
         for (int h = 0; h < MAX_GROUP; ++h) {
+          v[h] = 0.f;
           if (h < g) {
             uint32_t w[CQL / 2];
             if constexpr (CQL == 4) {
@@ -702,17 +703,37 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
             } else {
               w[0] = lds_u32(qh0 + h * D * 2);
             }
-            float part = 0.f;
 #pragma unroll
             for (int i = 0; i < CQL; ++i) {
               const float qv = __uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16));
-              part += fmaxf(qv * mnv[i], qv * mxv[i]);
+              v[h] += fmaxf(qv * mnv[i], qv * mxv[i]);
             }
-            const float U = warp_sum(part) * p.scale_log2;
-            if (h == 2 * qd) sc0 = U;
-            if (h == 2 * qd + 1) sc1 = U;
           }
         }
+        // transpose-reduce the 8 per-head partial sums over the warp (9 shuffles instead of
+        // 8 x 5): afterwards lane l holds head ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool hi = lane & 16;
+          const float send = hi ? v[i] : v[i + 4], keep = hi ? v[i + 4] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const bool hi = lane & 8;
+          const float send = hi ? v[i] : v[i + 2], keep = hi ? v[i + 2] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const bool hi = lane & 4;
+          const float send = hi ? v[0] : v[1], keep = hi ? v[1] : v[0];
+          v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+        auto lane_of = [](int h) { return ((h >> 2) & 1) << 4 | ((h >> 1) & 1) << 3 | (h & 1) << 2; };
+        sc0 = __shfl_sync(0xffffffffu, v[0], lane_of(2 * qd)) * p.scale_log2;
+        sc1 = __shfl_sync(0xffffffffu, v[0], lane_of(2 * qd + 1)) * p.scale_log2;
       }
       if (lane < 4) {  // a4: page score per head ("a single attention score per page", :147)
         float* pmx = p.pmax + (size_t)(unit * C + page) * g;
