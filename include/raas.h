@@ -96,6 +96,15 @@ RAAS_API int raas_create(const raas_config* cfg, void* arena, size_t arena_bytes
  * The prompt's attention output is not computed here (that is the model's prefill). */
 RAAS_API int raas_prefill(raas_handle* h, const void* k, const void* v, int32_t P, void* stream);
 
+/* Variable prompt lengths: request b's prompt is the first P_host[b] tokens of
+ * k, v laid out [batch][n_kv_heads][P_max][head_dim] (the rest is padding, never read).  Each
+ * request gets its own pinned pages and clock (t = P_host[b]).  P_host is a host array of
+ * `batch` int32; it is copied into the handle, so it may be released on return.  Errors as
+ * raas_prefill, RAAS_E_BUDGET if any request's prompt leaves it no decode page.
+ * raas_prefill(h, k, v, P, s) is raas_prefill_varlen with every P_host[b] = P_max = P. */
+RAAS_API int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int32_t* P_host,
+                                 int32_t P_max, void* stream);
+
 /* One decode step for every unit of the handle:
  *   t += 1; pick the slot (current page, else a fresh page, else the victim chosen at the end
  *   of the previous step = argmin over unpinned pages of (ts, start_pos)); write k_new/v_new

@@ -63,6 +63,7 @@ def lib():
         l.raas_ref_destroy.argtypes = [P]
         l.raas_ref_destroy.restype = None
         l.raas_ref_prefill.argtypes = [P, P, P, ctypes.c_int32]
+        l.raas_ref_prefill_varlen.argtypes = [P, P, P, P, ctypes.c_int32]
         l.raas_ref_decode_step.argtypes = [P, P, P, P, P]
         l.raas_ref_step_stamps.argtypes = [P, P]
         l.raas_ref_get_state.argtypes = [P, P, P, P, P, P]
@@ -127,6 +128,13 @@ class Oracle:
         rc = lib().raas_ref_prefill(self._h, _ptr(k), _ptr(v), int(P))
         if rc:
             raise OracleError(rc, "raas_ref_prefill")
+
+    def prefill_varlen(self, k_bits, v_bits, P_per_request):
+        P = np.ascontiguousarray(P_per_request, dtype=np.int32)
+        k, v = self._u16(k_bits), self._u16(v_bits)
+        rc = lib().raas_ref_prefill_varlen(self._h, _ptr(k), _ptr(v), _ptr(P), int(k.shape[2]))
+        if rc:
+            raise OracleError(rc, "raas_ref_prefill_varlen")
 
     def decode_step(self, q_bits, k_bits, v_bits, want_out=True):
         q, k, v = self._u16(q_bits), self._u16(k_bits), self._u16(v_bits)

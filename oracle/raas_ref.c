@@ -113,36 +113,51 @@ void raas_ref_destroy(raas_ref* h) {
 }
 
 /* Prefill (§2.1 :46 "computing and caching the key and value vectors for each
- * token"; App. B :396 prefill pages exempt).  Positions 1..P, 16 per page (:147). */
-int raas_ref_prefill(raas_ref* h, const uint16_t* k, const uint16_t* v, int32_t P) {
-  if (!h || P < 0 || (P > 0 && (!k || !v))) return REF_E_INVALID;
+ * token"; App. B :396 prefill pages exempt).  Positions 1..P_b, 16 per page (:147); request b
+ * keeps the first P[b] of its P_max rows. */
+int raas_ref_prefill_varlen(raas_ref* h, const uint16_t* k, const uint16_t* v, const int32_t* P,
+                            int32_t P_max) {
+  if (!h || !P || P_max < 0 || (P_max > 0 && (!k || !v))) return REF_E_INVALID;
   if (h->prefilled) return REF_E_STATE;
   const int32_t page = h->cfg.page, d = h->cfg.head_dim, C = h->C;
-  const int32_t Pp = (P + page - 1) / page;
-  if (Pp >= C) return REF_E_BUDGET;               /* D14: at least one decode page */
+  for (int32_t b = 0; b < h->cfg.batch; ++b) {
+    if (P[b] < 0 || P[b] > P_max) return REF_E_INVALID;
+    if ((P[b] + page - 1) / page >= C) return REF_E_BUDGET;  /* D14: a decode page per unit */
+  }
   for (int32_t ui = 0; ui < h->units; ++ui) {
     ref_unit* u = &h->u[ui];
-    for (int32_t j = 0; j < P; ++j) {             /* token j has position j+1 */
+    const int32_t Pu = P[ui / h->cfg.n_kv_heads];
+    const int32_t Pp = (Pu + page - 1) / page;
+    for (int32_t j = 0; j < Pu; ++j) {            /* token j has position j+1 */
       int32_t p = j / page, off = j % page;
       for (int32_t c = 0; c < d; ++c) {
-        u->K[((size_t)p * page + off) * d + c] = widen_bf16(k[((size_t)ui * P + j) * d + c]);
-        u->V[((size_t)p * page + off) * d + c] = widen_bf16(v[((size_t)ui * P + j) * d + c]);
+        u->K[((size_t)p * page + off) * d + c] = widen_bf16(k[((size_t)ui * P_max + j) * d + c]);
+        u->V[((size_t)p * page + off) * d + c] = widen_bf16(v[((size_t)ui * P_max + j) * d + c]);
       }
     }
     for (int32_t p = 0; p < Pp; ++p) {
       u->start[p] = p * page + 1;
-      u->count[p] = (P - p * page) < page ? (P - p * page) : page;
+      u->count[p] = (Pu - p * page) < page ? (Pu - p * page) : page;
       u->ts[p] = 0;                               /* D17: pinned pages' ts untracked */
       u->pinned[p] = 1;
     }
     u->used = Pp;
     u->cur = Pp - 1;                              /* -1 when P == 0 */
-    u->t = P;
+    u->t = Pu;
     u->evicted = -1;
     u->slot = -1;
   }
   h->prefilled = 1;
   return REF_OK;
+}
+
+int raas_ref_prefill(raas_ref* h, const uint16_t* k, const uint16_t* v, int32_t P) {
+  if (!h || P < 0) return REF_E_INVALID;
+  int32_t* Ps = (int32_t*)malloc(sizeof(int32_t) * (size_t)h->cfg.batch);
+  for (int32_t b = 0; b < h->cfg.batch; ++b) Ps[b] = P;
+  const int rc = raas_ref_prefill_varlen(h, k, v, Ps, P);
+  free(Ps);
+  return rc;
 }
 
 /* Slot selection and in-place write for one unit (D9-D13).

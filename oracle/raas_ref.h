@@ -50,6 +50,10 @@ typedef struct raas_ref raas_ref;
 int  raas_ref_create(const raas_ref_config* cfg, raas_ref** out);
 void raas_ref_destroy(raas_ref* h);
 int  raas_ref_prefill(raas_ref* h, const uint16_t* k, const uint16_t* v, int32_t P);
+/* variable prompt lengths: k, v [batch][n_kv_heads][P_max][head_dim]; request b keeps its first
+ * P[b] tokens.  raas_ref_prefill == every P[b] = P_max = P. */
+int  raas_ref_prefill_varlen(raas_ref* h, const uint16_t* k, const uint16_t* v, const int32_t* P,
+                             int32_t P_max);
 /* one decode step for every unit; out may be NULL */
 int  raas_ref_decode_step(raas_ref* h, const uint16_t* q, const uint16_t* k_new,
                           const uint16_t* v_new, double* out);

@@ -52,7 +52,7 @@ template <int D>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
-  size_t kvstore, ts, start, cnt, npin, plan, counter, pmax, part_acc, part_ml, status,
+  size_t kvstore, ts, start, cnt, npin, plen, plan, counter, pmax, part_acc, part_ml, status,
       stats, sq, sk, sv, so, total;
 };
 
@@ -101,6 +101,7 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.start = take(U * C * 4);
   L.cnt = take(U * C * 4);
   L.npin = take(U * 4);
+  L.plen = take((size_t)c->batch * 4);
   L.plan = take(U * 16);
   L.counter = take(U * 4);
   L.pmax = take(U * C * g * 4);
@@ -172,6 +173,7 @@ struct raas_handle {
   int smem;
   uint8_t* arena;
   int prefilled;
+  std::vector<int32_t> plen_host;  // prompt lengths, kept alive for the async upload
 };
 
 namespace {
@@ -328,41 +330,58 @@ int raas_destroy(raas_handle* h) {
   return RAAS_OK;
 }
 
-int raas_prefill(raas_handle* h, const void* k, const void* v, int32_t P, void* stream) {
+int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int32_t* P_host,
+                        int32_t P_max, void* stream) {
   if (!h) return fail(RAAS_E_INVALID, "null handle");
   if (h->prefilled) return fail(RAAS_E_STATE, "handle already prefilled");
-  if (P < 0) return fail(RAAS_E_INVALID, "P < 0");
-  const int Pp = (P + raas::PAGE - 1) / raas::PAGE;
-  if (Pp >= h->d.C) return fail(RAAS_E_BUDGET, "ceil(P/16)=%d leaves no decode page (C=%d)", Pp, h->d.C);
-  if (P > 0 && (!k || !v || !aligned16(k) || !aligned16(v)))
+  if (!P_host || P_max < 0) return fail(RAAS_E_INVALID, "bad prompt lengths");
+  const int B = h->cfg.batch;
+  for (int b = 0; b < B; ++b) {
+    if (P_host[b] < 0 || P_host[b] > P_max)
+      return fail(RAAS_E_INVALID, "P[%d]=%d outside [0, P_max=%d]", b, P_host[b], P_max);
+    const int Pp = (P_host[b] + raas::PAGE - 1) / raas::PAGE;
+    if (Pp >= h->d.C)
+      return fail(RAAS_E_BUDGET, "request %d: ceil(P/16)=%d leaves no decode page (C=%d)", b, Pp, h->d.C);
+  }
+  if (P_max > 0 && (!k || !v || !aligned16(k) || !aligned16(v)))
     return fail(RAAS_E_INVALID, "k/v must be non-null 16-byte aligned device pointers");
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* a = h->arena;
   auto* kvs = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kvstore);
-  if (P > 0) {
-    const size_t total = (size_t)h->d.units * P * (h->cfg.head_dim / 8);
+  auto* plen = reinterpret_cast<int32_t*>(a + h->lay.plen);
+  h->plen_host.assign(P_host, P_host + B);
+  RAAS_CUDA(cudaMemcpyAsync(plen, h->plen_host.data(), (size_t)B * 4, cudaMemcpyHostToDevice, st));
+  if (P_max > 0) {
+    const size_t total = (size_t)h->d.units * P_max * (h->cfg.head_dim / 8);
     const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)h->num_sms * 16);
     if (h->cfg.head_dim == 128)
       raas::raas_prefill_copy<128><<<blocks, 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs,
-          h->d.units, P, h->d.C);
+          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs, plen,
+          h->d.units, h->cfg.n_kv_heads, P_max, h->d.C);
     else
       raas::raas_prefill_copy<64><<<blocks, 256, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs,
-          h->d.units, P, h->d.C);
+          static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs, plen,
+          h->d.units, h->cfg.n_kv_heads, P_max, h->d.C);
     RAAS_CUDA(cudaGetLastError());
   }
   const size_t n = (size_t)h->d.units * h->d.C;
   raas::raas_meta_init<<<(int)std::min<size_t>((n + 255) / 256, 4096), 256, 0, st>>>(
       reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
       reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
-      reinterpret_cast<int4*>(a + h->lay.plan), h->d.units, h->d.C, P);
+      reinterpret_cast<int4*>(a + h->lay.plan), plen, h->d.units, h->cfg.n_kv_heads, h->d.C);
   RAAS_CUDA(cudaGetLastError());
   int rc = refresh(h, st);
   if (rc) return rc;
   h->prefilled = 1;
   return RAAS_OK;
+}
+
+int raas_prefill(raas_handle* h, const void* k, const void* v, int32_t P, void* stream) {
+  if (!h) return fail(RAAS_E_INVALID, "null handle");
+  if (P < 0) return fail(RAAS_E_INVALID, "P < 0");
+  std::vector<int32_t> plens((size_t)h->cfg.batch, P);
+  return raas_prefill_varlen(h, k, v, plens.data(), P, stream);
 }
 
 int raas_decode_step(raas_handle* h, const void* q, const void* k_new, const void* v_new,

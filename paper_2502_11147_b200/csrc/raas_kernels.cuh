@@ -97,15 +97,18 @@ namespace raas {
 template <int D>
 __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
                                   const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kvstore,
-                                  int units, int P, int C) {
+                                  const int32_t* __restrict__ plen, int units, int n_kv_heads,
+                                  int P_max, int C) {
+  // k, v: [units][P_max][D]; unit u = (b, kv-head) copies its request's first plen[b] tokens
   constexpr int NCH = D / 8;
-  const size_t total = (size_t)units * P * NCH;
+  const size_t total = (size_t)units * P_max * NCH;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % NCH);
-    const size_t src = i / NCH;  // unit * P + j
-    const int j = (int)(src % P);
-    const size_t u = src / P;
+    const size_t src = i / NCH;  // unit * P_max + j
+    const int j = (int)(src % P_max);
+    const size_t u = src / P_max;
+    if (j >= plen[u / n_kv_heads]) continue;
     const int r = j % PAGE;
     const size_t dst = ((u * C + j / PAGE) * 2 * PAGE + r) * D + (ch ^ (r & 7)) * 8;
     *reinterpret_cast<uint4*>(kvstore + dst) =
@@ -115,19 +118,22 @@ __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
   }
 }
 
-// metadata after prefill: pages < Pp pinned and full (the last may be partial), t = P
+// metadata after prefill: unit u's pages < Pp(u) pinned and full (the last may be partial),
+// t = P(u), with P(u) = plen[u / n_kv_heads] (variable prompt lengths, NEXT-2)
 __global__ void raas_meta_init(int32_t* ts, int32_t* start, int32_t* cnt, int32_t* npin,
-                               int4* plan, int units, int C, int P) {
-  const int Pp = (P + PAGE - 1) / PAGE;
+                               int4* plan, const int32_t* __restrict__ plen, int units,
+                               int n_kv_heads, int C) {
   const size_t total = (size_t)units * C;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int pg = (int)(i % C);
+    const size_t u = i / C;
+    const int P = plen[u / n_kv_heads];
+    const int Pp = (P + PAGE - 1) / PAGE;
     ts[i] = 0;
     start[i] = pg < Pp ? pg * PAGE + 1 : 0;
     cnt[i] = pg < Pp ? min(PAGE, P - pg * PAGE) : 0;
     if (pg == 0) {
-      const size_t u = i / C;
       npin[u] = Pp;
       plan[u] = make_int4(0, 0, 0, P + 1);  // .w = t + 1; the rest derived by raas_refresh
     }

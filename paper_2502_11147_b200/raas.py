@@ -63,6 +63,7 @@ def lib():
     l.raas_arena_bytes.restype = SZ
     l.raas_create.argtypes = [ctypes.POINTER(raas_config), V, SZ, I, ctypes.POINTER(V)]
     l.raas_prefill.argtypes = [V, V, V, ctypes.c_int32, V]
+    l.raas_prefill_varlen.argtypes = [V, V, V, V, ctypes.c_int32, V]
     l.raas_decode_step.argtypes = [V, V, V, V, V, V]
     l.raas_decode_step_host.argtypes = [V, V, V, V, V, V]
     l.raas_destroy.argtypes = [V]
@@ -74,7 +75,7 @@ def lib():
     l.raas_launch_info.argtypes = [V, V]
     l.raas_last_error.argtypes = []
     l.raas_last_error.restype = ctypes.c_char_p
-    for n in ("raas_create", "raas_prefill", "raas_decode_step", "raas_decode_step_host",
+    for n in ("raas_create", "raas_prefill", "raas_prefill_varlen", "raas_decode_step", "raas_decode_step_host",
               "raas_destroy", "raas_get_state", "raas_set_state", "raas_get_kv",
               "raas_get_status", "raas_get_counters", "raas_launch_info"):
         getattr(l, n).restype = I
@@ -160,6 +161,13 @@ class RaasLayer:
         P = k.shape[2] if P is None else P
         _check(lib().raas_prefill(self._h, _dptr(k), _dptr(v), int(P), _stream_ptr(stream)),
                "raas_prefill")
+
+    def raas_prefill_varlen(self, k, v, P_per_request, stream=None):
+        """k, v: [batch, n_kv_heads, P_max, head_dim]; request b uses its first P[b] tokens."""
+        P = np.ascontiguousarray(P_per_request, dtype=np.int32)
+        assert P.shape == (self.batch,)
+        _check(lib().raas_prefill_varlen(self._h, _dptr(k), _dptr(v), _np_ptr(P), int(k.shape[2]),
+                                         _stream_ptr(stream)), "raas_prefill_varlen")
 
     def raas_decode_step(self, q, k_new, v_new, out, stream=None):
         _check(lib().raas_decode_step(self._h, _dptr(q), _dptr(k_new), _dptr(v_new), _dptr(out),

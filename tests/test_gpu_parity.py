@@ -415,3 +415,20 @@ def test_quest_stamps_superset_of_exact_on_gpu():
     t_now = (P + 1 + np.arange(T))[:, None, None]
     ex, qu = states[0] == t_now, states[1] == t_now
     assert (qu | ~ex).all() and (qu & ~ex).any()
+
+
+# ------------------------------------------------------------------ NEXT-2: variable prompts
+
+
+def test_varlen_prefill_lockstep(oracle_mod):
+    """Per-request prompt lengths (raas_prefill_varlen) against the oracle's varlen prefill."""
+    B, Hq, Hkv, d, Pmax, T, L = 4, 8, 2, 128, 70, 260, 192
+    Ps = [70, 33, 1, 0]
+    st = waterfall_stream(55, B, Hq, Hkv, d, Pmax, T)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_prefill_varlen(to_dev(st.k_pre), to_dev(st.v_pre), Ps)
+    orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, batch=B)
+    orc.prefill_varlen(st.k_pre, st.v_pre, Ps)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, layer=layer, oracle=orc)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
+    assert layer.raas_get_state()["t"].tolist() == [P + T for P in Ps for _ in range(Hkv)]

@@ -488,3 +488,31 @@ def test_quest_bound_is_exact_for_identical_keys(oracle_mod):
     ex = _dense_pstars(oracle_mod, short, 2, 0)
     qu = _dense_pstars(oracle_mod, short, 2, 1)
     assert np.allclose(qu, ex, rtol=1e-12, atol=0)
+
+
+# ---------------------------------------------------------------- NEXT-2: variable prompts
+
+
+def test_varlen_prefill_equals_independent_requests(oracle_mod):
+    """Requests with different prompt lengths in one batch behave exactly like separate
+    single-request runs (units are independent, reading D5): same state, same outputs."""
+    B, Hq, Hkv, d, Pmax, T, L = 3, 8, 2, 32, 50, 120, 96
+    Ps = [50, 17, 0]
+    st = waterfall_stream(23, B, Hq, Hkv, d, Pmax, T)
+    o = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, batch=B)
+    o.prefill_varlen(st.k_pre, st.v_pre, Ps)
+    singles = []
+    for b, P in enumerate(Ps):
+        s1 = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, batch=1)
+        s1.prefill(np.ascontiguousarray(st.k_pre[b:b + 1, :, :P]), np.ascontiguousarray(st.v_pre[b:b + 1, :, :P]), P)
+        singles.append(s1)
+    for i in range(T):
+        out = o.decode_step(st.q[i], st.k[i], st.v[i])
+        stv = o.get_state()
+        for b, s1 in enumerate(singles):
+            o1 = s1.decode_step(st.q[i][b:b + 1], st.k[i][b:b + 1], st.v[i][b:b + 1])
+            assert np.array_equal(out[b:b + 1], o1)
+            s1s = s1.get_state()
+            for k in ("t", "ts", "start", "count", "pinned"):
+                assert np.array_equal(stv[k][b * Hkv:(b + 1) * Hkv], s1s[k])
+    assert o.get_state()["t"].tolist() == [P + T for P in Ps for _ in range(Hkv)]
