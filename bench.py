@@ -226,7 +226,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     gen.manual_seed(1000 * args.config + rank)
     sp = args.split_pages if args.split_pages else cfg.get("split_pages", 0)
     score_mode = 1 if args.score == "quest" else 0
-    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode)
+    layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode,
+                        stamp_rule=1 if args.top_r > 0 else 0, top_r=args.top_r)
               for _ in range(nl)]
     info = layers[0].raas_launch_info()
     for ly in layers:
@@ -394,6 +395,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
                    "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
                    "page": 16, "alpha": args.alpha, "score_mode": args.score,
+                   "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
                    "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
                                    if heads else f"request-sharded x{world}, no collective"),
                    "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
@@ -473,6 +475,8 @@ def main():
     ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
                     help="multi-GPU: shard requests (weak scaling) or kv-heads (strong, all-gather)")
     ap.add_argument("--split-pages", type=int, default=0, help="override pages per split tile")
+    ap.add_argument("--top-r", type=float, default=0.0,
+                    help="stamp the top r fraction of pages instead of the alpha threshold (NEXT-3)")
     ap.add_argument("--score", default="exact", choices=["exact", "quest"],
                     help="page score for stamping: exact page max (D4) or Quest bound (NEXT-1)")
     ap.add_argument("--dense", type=int, default=0,

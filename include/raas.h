@@ -78,6 +78,13 @@ typedef struct {
                                 :147-151, App. B :362): per channel c, max(q_c min_c, q_c max_c)
                                 over the page's keys, summed, scaled and normalised by the step's
                                 LSE (reading D22).  A superset of mode 0's stamps. */
+  int32_t stamp_rule;    /* 0 = stamp iff score > alpha (the default, :29, :169);
+                            1 = top-r (PAPER.md :135, "assign the latest timestamp to r=50% tokens
+                                with the highest attention scores in each decoding step"): per
+                                unit and step, the k = ceilf(top_r * n) highest-scored of the n
+                                unpinned resident pages, ties to the oldest page (reading D23).
+                                Needs L <= 8192. */
+  float   top_r;         /* r in [0, 1] for stamp_rule 1 (0.5 in the paper) */
 } raas_config;
 
 /* Bytes of device memory the handle needs (KV store: per unit L/16 pages, each 16 K rows + 16 V

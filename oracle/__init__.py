@@ -48,6 +48,8 @@ class _Cfg(ctypes.Structure):
         ("batch", ctypes.c_int32),
         ("softmax_scale", ctypes.c_double),
         ("score_mode", ctypes.c_int32),
+        ("stamp_rule", ctypes.c_int32),
+        ("top_r", ctypes.c_double),
     ]
 
 
@@ -93,9 +95,9 @@ class Oracle:
     """fp64 RaaS state machine over `batch * n_kv_heads` independent units (host)."""
 
     def __init__(self, L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch,
-                 softmax_scale=0.0, score_mode=0):
+                 softmax_scale=0.0, score_mode=0, stamp_rule=0, top_r=0.5):
         self.cfg = _Cfg(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
-                        score_mode)
+                        score_mode, stamp_rule, top_r)
         self.C = L // page if page > 0 else 0
         self.units = batch * n_kv_heads
         self.page, self.d, self.hq, self.hkv, self.batch = page, head_dim, n_q_heads, n_kv_heads, batch

@@ -75,6 +75,8 @@ int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
   if (cfg->head_dim <= 0 || cfg->batch <= 0) return REF_E_INVALID;
   if (!(cfg->alpha >= 0.0)) return REF_E_INVALID;
   if (cfg->score_mode != 0 && cfg->score_mode != 1) return REF_E_INVALID;
+  if (cfg->stamp_rule != 0 && cfg->stamp_rule != 1) return REF_E_INVALID;
+  if (cfg->stamp_rule == 1 && !(cfg->top_r >= 0.0 && cfg->top_r <= 1.0)) return REF_E_INVALID;
   raas_ref* h = (raas_ref*)calloc(1, sizeof *h);
   if (!h) return REF_E_INVALID;
   h->cfg = *cfg;
@@ -276,11 +278,39 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
   /* stamp: "we assign it the latest timestamp" when the score is above alpha (:29, :98,
    * :364), strictly (D3), in the log domain s - LSE > ln(alpha) (D2). */
   const double ln_alpha = log(h->cfg.alpha);     /* alpha = 0 -> -inf: every page stamped */
-  for (int32_t p = 0; p < C; ++p) {
-    u->pstar[p] = -1.0;
-    if (u->pinned[p] || u->count[p] == 0) continue;
-    u->pstar[p] = exp(best[p]);
-    if (best[p] > ln_alpha) u->ts[p] = u->t;
+  if (h->cfg.stamp_rule == 0) {
+    for (int32_t p = 0; p < C; ++p) {
+      u->pstar[p] = -1.0;
+      if (u->pinned[p] || u->count[p] == 0) continue;
+      u->pstar[p] = exp(best[p]);
+      if (best[p] > ln_alpha) u->ts[p] = u->t;
+    }
+  } else {
+    /* top-r (:135): "assign the latest timestamp to r=50% tokens with the highest attention
+     * scores in each decoding step", at page level over the unpinned resident pages (D23):
+     * k = ceilf(r * n) pages, ranked by score, ties to the smaller start_pos.  Selection by
+     * repeated maximum (plain, O(n k)). */
+    int32_t n = 0;
+    for (int32_t p = 0; p < C; ++p) {
+      u->pstar[p] = -1.0;
+      if (u->pinned[p] || u->count[p] == 0) continue;
+      u->pstar[p] = exp(best[p]);
+      n++;
+    }
+    int32_t k = (int32_t)ceilf((float)h->cfg.top_r * (float)n);
+    if (k > n) k = n;
+    uint8_t* taken = (uint8_t*)calloc((size_t)C, 1);
+    for (int32_t r = 0; r < k; ++r) {
+      int32_t arg = -1;
+      for (int32_t p = 0; p < C; ++p) {
+        if (u->pinned[p] || u->count[p] == 0 || taken[p]) continue;
+        if (arg < 0 || best[p] > best[arg] || (best[p] == best[arg] && u->start[p] < u->start[arg]))
+          arg = p;
+      }
+      taken[arg] = 1;
+      u->ts[arg] = u->t;
+    }
+    free(taken);
   }
   free(s); free(best); free(qh);
 }

@@ -43,6 +43,10 @@ typedef struct {
                                 :362): U_p = sum_c max(q_c min_c, q_c max_c) over the per-channel
                                 min / max of the page's keys, estimated score exp(scale U_p - LSE)
                                 (reading D22; "parity unpinned": the paper gives no formula) */
+  int32_t stamp_rule;    /* 0 = stamp iff score > alpha; 1 = top-r (§3.2 :135): stamp
+                            the k = ceilf(top_r * n) best-scored of the n unpinned resident pages,
+                            ranked by (score desc, start_pos asc) (reading D23) */
+  double  top_r;
 } raas_ref_config;
 
 typedef struct raas_ref raas_ref;

@@ -70,12 +70,17 @@ int derive(const raas_config* c, Derived* d) {
   if (!(c->alpha >= 0.f)) return fail(RAAS_E_INVALID, "alpha must be >= 0");
   if (c->softmax_scale < 0.f) return fail(RAAS_E_INVALID, "softmax_scale must be >= 0");
   if (c->score_mode != 0 && c->score_mode != 1) return fail(RAAS_E_INVALID, "score_mode must be 0 or 1");
+  if (c->stamp_rule != 0 && c->stamp_rule != 1) return fail(RAAS_E_INVALID, "stamp_rule must be 0 or 1");
+  if (c->stamp_rule == 1 && !(c->top_r >= 0.f && c->top_r <= 1.f))
+    return fail(RAAS_E_INVALID, "top_r must be in [0, 1]");
   if (c->page != raas::PAGE) return fail(RAAS_E_UNSUPPORTED, "page must be 16");
   if (c->head_dim != 64 && c->head_dim != 128)
     return fail(RAAS_E_UNSUPPORTED, "head_dim must be 64 or 128");
   d->g = c->n_q_heads / c->n_kv_heads;
   if (d->g > raas::MAX_GROUP) return fail(RAAS_E_UNSUPPORTED, "GQA group > 8");
   d->C = c->L / c->page;
+  if (c->stamp_rule == 1 && d->C > 512)
+    return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports L <= 8192 (512 pages)");
   d->units = c->batch * c->n_kv_heads;
   if ((long long)d->units * d->C * raas::PAGE >= (1LL << 31))
     return fail(RAAS_E_UNSUPPORTED, "units * L too large for 32-bit TMA row coordinates");
@@ -205,6 +210,8 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.split_pages = h->d.split_pages;
   p.g = h->d.g;
   p.score_mode = h->cfg.score_mode;
+  p.stamp_rule = h->cfg.stamp_rule;
+  p.top_r = h->cfg.top_r;
   const float scale = h->cfg.softmax_scale > 0.f ? h->cfg.softmax_scale
                                                  : 1.0f / sqrtf((float)h->cfg.head_dim);
   p.scale_log2 = scale * 1.4426950408889634f;

@@ -264,6 +264,96 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
   float lse[MAX_GROUP];
 #pragma unroll
   for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
+  // page score x_p = max_h (score_hp - LSE_h) (log2 domain).  Rule 0: stamp iff x_p > log2 a
+  // (strict, D3).  Rule 1 (top-r, PAPER.md :135, reading D23): stamp the k = ceil(r n) pages with
+  // the largest (x_p, -start_pos) among the n unpinned resident pages.
+  auto page_x = [&](int i) {
+    float x = -INFINITY;
+#pragma unroll
+    for (int h = 0; h < MAX_GROUP; ++h)
+      if (h < g) x = fmaxf(x, pmv[i][h] - lse[h]);
+    return x;
+  };
+  auto page_key = [&](float x, int st) {  // larger key = ranked first; valid keys are > 0
+    const uint32_t b = __float_as_uint(x);
+    const uint32_t sx = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return (static_cast<unsigned long long>(sx) << 32) | (0xffffffffu - static_cast<uint32_t>(st));
+  };
+  unsigned long long kth = 0;
+  if (p.stamp_rule == 1) {
+    // pass 1: keys of the decision pages -> scratch (the split weights are no longer needed)
+    const uint32_t scr_key = scr, scr_hist = scr + 8 * 512;
+    int nd = 0;
+    for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
+      if (pc > 0) load_meta(pc);
+#pragma unroll
+      for (int i = 0; i < PPL; ++i) {
+        const int pg = pc + 32 * i + lane;
+        if (pg < used_eff) {
+          const int st_p = (pg == slot && off == 0) ? t : stv[i];
+          const unsigned long long key = pg >= npin ? page_key(page_x(i), st_p) : 0ull;
+          nd += pg >= npin ? 1 : 0;
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(scr_key + 8 * pg), "l"(key) : "memory");
+        }
+      }
+    }
+    nd = warp_sum_i(nd);
+    int krem = (int)ceilf(p.top_r * (float)nd);  // fp32, as the oracle (D23)
+    krem = krem < 0 ? 0 : (krem > nd ? nd : krem);
+    __syncwarp();
+    if (krem > 0) {
+      // radix select of the krem-th largest 64-bit key, 8 bits per pass, smem histogram
+      unsigned long long prefix = 0, mask = 0;
+      for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sts_f32(scr_hist + 4 * (lane * 8 + j), 0.f);
+        __syncwarp();
+        for (int pg = lane; pg < used_eff; pg += 32) {
+          unsigned long long key;
+          asm volatile("ld.shared.u64 %0, [%1];" : "=l"(key) : "r"(scr_key + 8 * pg));
+          if (key != 0 && (key & mask) == prefix)
+            atomicAdd(reinterpret_cast<int*>(__cvta_shared_to_generic(scr_hist)) +
+                          ((key >> shift) & 255), 1);
+        }
+        __syncwarp();
+        // bins in descending digit order: lane l owns digits 255-8l .. 248-8l
+        int c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          c[j] = __float_as_int(lds_f32(scr_hist + 4 * (255 - (lane * 8 + j))));
+          tot += c[j];
+        }
+        int incl = tot;  // inclusive prefix over lanes (higher digits first)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int excl = incl - tot;
+        const unsigned hit = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
+        const int src = __ffs(hit) - 1;
+        int digit = 0, above = 0;
+        if (lane == src) {
+          int run = excl;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (run + c[j] >= krem) { digit = 255 - (lane * 8 + j); above = run; break; }
+            run += c[j];
+          }
+        }
+        digit = __shfl_sync(0xffffffffu, digit, src);
+        above = __shfl_sync(0xffffffffu, above, src);
+        krem -= above;
+        prefix |= static_cast<unsigned long long>(digit) << shift;
+        mask |= 255ull << shift;
+        __syncwarp();
+      }
+      kth = prefix;  // keys are unique (start positions differ): exactly k keys are >= kth
+    } else {
+      kth = ~0ull;  // nothing stamped
+    }
+    if (used_eff > 32 * PPL) load_meta(0);
+  }
   Cand best{~0ull, -1};
   int n_stamp = 0, n_dec = 0;
   for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
@@ -280,11 +370,9 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
           p.cnt[ix] = off + 1;
         }
         if (pg >= npin) {
-          float x = -INFINITY;
-#pragma unroll
-          for (int h = 0; h < MAX_GROUP; ++h)
-            if (h < g) x = fmaxf(x, pmv[i][h] - lse[h]);
-          const bool stamp = x > p.log2_alpha;  // strict (D3)
+          const float x = page_x(i);
+          const bool stamp = p.stamp_rule == 1 ? page_key(x, st_p) >= kth
+                                               : x > p.log2_alpha;  // strict (D3)
           ++n_dec;
           n_stamp += stamp ? 1 : 0;
           if (stamp || is_slot) { ts_p = t; p.ts[ix] = t; }  // stamp, or write refresh (D8)

@@ -46,6 +46,8 @@ struct DecodeParams {
   unsigned long long* stats;  // [4]: stamps, decisions, evictions, unit-steps
   int units, C, nsplit, split_pages, g;
   int score_mode;    // 0 exact page max (D4), 1 Quest representative-key bound (D22)
+  int stamp_rule;    // 0 threshold alpha (D2/D3), 1 top-r fraction of pages (D23)
+  float top_r;
   float scale_log2;  // softmax_scale * log2(e)
   float log2_alpha;  // log2(alpha); -inf for alpha == 0
 };

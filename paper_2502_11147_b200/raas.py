@@ -35,6 +35,8 @@ class raas_config(ctypes.Structure):
         ("softmax_scale", ctypes.c_float),
         ("split_pages", ctypes.c_int32),
         ("score_mode", ctypes.c_int32),
+        ("stamp_rule", ctypes.c_int32),
+        ("top_r", ctypes.c_float),
     ]
 
 
@@ -95,12 +97,14 @@ def _check(rc, what):
 
 
 SCORE_EXACT, SCORE_QUEST = 0, 1
+STAMP_ALPHA, STAMP_TOP_R = 0, 1
 
 
 def make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch, page=16, softmax_scale=0.0,
-                split_pages=0, score_mode=SCORE_EXACT) -> raas_config:
+                split_pages=0, score_mode=SCORE_EXACT, stamp_rule=STAMP_ALPHA,
+                top_r=0.5) -> raas_config:
     return raas_config(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
-                       split_pages, score_mode)
+                       split_pages, score_mode, stamp_rule, top_r)
 
 
 def raas_arena_bytes(cfg: raas_config) -> int:
@@ -131,12 +135,13 @@ class RaasLayer:
     """One libraas handle (one attention layer of `batch` requests) plus its device arena."""
 
     def __init__(self, L, alpha, n_q_heads, n_kv_heads, head_dim, batch, device=None,
-                 softmax_scale=0.0, split_pages=0, score_mode=SCORE_EXACT):
+                 softmax_scale=0.0, split_pages=0, score_mode=SCORE_EXACT,
+                 stamp_rule=STAMP_ALPHA, top_r=0.5):
         import torch
 
         self.cfg = make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch,
                                softmax_scale=softmax_scale, split_pages=split_pages,
-                               score_mode=score_mode)
+                               score_mode=score_mode, stamp_rule=stamp_rule, top_r=top_r)
         self.device = torch.device(device if device is not None else "cuda")
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         nbytes = raas_arena_bytes(self.cfg)

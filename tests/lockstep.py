@@ -34,7 +34,18 @@ class LockstepResult:
         self.gpu_evictions = []   # per step, list of (unit, evicted start_pos)
 
 
-def compare_state(g, o, alpha, pstar, res, layer, resync=True):
+def _topr_band(pstar_u, p, top_r):
+    """top-r rule: a differing decision is allowed only at the k-th boundary (the page's score
+    within 1e-6 relative of the oracle's k-th largest score)."""
+    dec = np.sort(pstar_u[pstar_u >= 0])[::-1]
+    k = int(np.ceil(np.float32(top_r) * np.float32(len(dec))))
+    if k == 0 or k > len(dec):
+        return False
+    kth = dec[k - 1]
+    return abs(pstar_u[p] - kth) <= 1e-6 * kth
+
+
+def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None):
     keys = ("t", "ts", "start", "count", "pinned")
     same = all(np.array_equal(g[k], o[k]) for k in keys)
     if same:
@@ -45,6 +56,10 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True):
     diff = np.argwhere(g["ts"] != o["ts"])
     for u, p in diff:
         ps = pstar[u, p]
+        if top_r is not None:
+            assert _topr_band(pstar[u], p, top_r), f"top-r decision differs at unit {u} page {p}"
+            res.band_events += 1
+            continue
         assert ps >= 0 and abs(ps - alpha) < BAND, (
             f"ts differs at unit {u} page {p}: gpu {g['ts'][u, p]} oracle {o['ts'][u, p]}, "
             f"p*={ps!r} outside the |p*-alpha|<{BAND} band")
@@ -54,16 +69,18 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True):
 
 
 def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_every=1,
-                 layer=None, oracle=None, device="cuda", on_step=None, score_mode=0):
+                 layer=None, oracle=None, device="cuda", on_step=None, score_mode=0,
+                 stamp_rule=0, top_r=0.5):
     """Drive both sides through the whole stream; returns LockstepResult."""
     B, _, P, d = stream.k_pre.shape
     if layer is None:
         layer = RaasLayer(L, alpha, Hq, Hkv, d, B, device=device, split_pages=split_pages,
-                          score_mode=score_mode)
+                          score_mode=score_mode, stamp_rule=stamp_rule, top_r=top_r)
         layer.raas_prefill(to_dev(stream.k_pre, device), to_dev(stream.v_pre, device), P)
     if oracle is None:
         oracle = oracle_mod.Oracle(L=L, alpha=alpha, page=16, n_q_heads=Hq, n_kv_heads=Hkv,
-                                   head_dim=d, batch=B, score_mode=score_mode)
+                                   head_dim=d, batch=B, score_mode=score_mode,
+                                   stamp_rule=stamp_rule, top_r=top_r)
         oracle.prefill(stream.k_pre, stream.v_pre, P)
     res = LockstepResult()
     out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=device)
@@ -82,7 +99,8 @@ def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_eve
         o_state = oracle.get_state()
         tr = oracle.get_trace()
         res.evictions += int((tr["evicted"] >= 0).sum())
-        compare_state(g_state, o_state, alpha, tr["pstar"], res, layer)
+        compare_state(g_state, o_state, alpha, tr["pstar"], res, layer,
+                      top_r=top_r if stamp_rule == 1 else None)
         if on_step is not None:
             on_step(i, layer, oracle, g_out, o_out)
     assert layer.raas_get_status() == 0

@@ -432,3 +432,23 @@ def test_varlen_prefill_lockstep(oracle_mod):
     res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, layer=layer, oracle=orc)
     assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
     assert layer.raas_get_state()["t"].tolist() == [P + T for P in Ps for _ in range(Hkv)]
+
+
+# ------------------------------------------------------------------ NEXT-3: top-r stamping
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,r,score", [
+    (2, 8, 2, 128, 40, 300, 256, 0, 0.5, 0),
+    (2, 28, 4, 128, 64, 200, 192, 4, 0.3, 0),
+    (1, 4, 2, 64, 32, 256, 64, 0, 0.5, 0),     # toy shapes
+    (2, 8, 2, 128, 40, 260, 256, 3, 0.5, 1),   # top-r over Quest scores
+])
+def test_top_r_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, r, score):
+    """stamp_rule = 1 (top-r, PAPER.md :135) against the oracle: bit-exact state (a differing
+    decision allowed only at the k-th boundary, counted: 0 here), out within 2e-2."""
+    st = waterfall_stream(400 + B + Hq + P, B, Hq, Hkv, d, P, T)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, split_pages=sp,
+                                 score_mode=score, stamp_rule=1, top_r=r)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
+    c = layer.raas_get_counters()
+    assert 0 < c["stamps"] < c["decisions"]

@@ -516,3 +516,84 @@ def test_varlen_prefill_equals_independent_requests(oracle_mod):
             for k in ("t", "ts", "start", "count", "pinned"):
                 assert np.array_equal(stv[k][b * Hkv:(b + 1) * Hkv], s1s[k])
     assert o.get_state()["t"].tolist() == [P + T for P in Ps for _ in range(Hkv)]
+
+
+# ---------------------------------------------------------------- NEXT-3: top-r stamping
+
+
+@pytest.mark.parametrize("r,closed", [(1.0, "alpha0"), (0.0, "alpha1")])
+def test_top_r_extremes_are_sliding_window(oracle_mod, r, closed):
+    """r = 1 stamps every decision page (= alpha 0), r = 0 none (= alpha >= 1): both reduce to
+    the StreamingLLM window of P4."""
+    P, L, T = 100, 128, 300
+    st = gaussian_stream(7, 1, 2, 1, 16, P, T)
+    o = oracle_mod.Oracle(L=L, alpha=0.5, page=PAGE, n_q_heads=2, n_kv_heads=1, head_dim=16,
+                          batch=1, stamp_rule=1, top_r=r)
+    o.prefill(st.k_pre, st.v_pre, P)
+    for i in range(T):
+        o.decode_step(st.q[i], st.k[i], st.v[i])
+        assert o.resident_positions(0).tolist() == sliding_window(P, L, P + i + 1)
+
+
+def brute_force_top_r(stream, L, r, page, g):
+    """From-scratch simulator of the top-r rule (PAPER.md :135, reading D23): each step, stamp
+    the ceil(r n) unpinned resident pages with the largest max-probability (ties to the oldest
+    page), direct exp/sum per step."""
+    K, V = positions_kv(stream)
+    B, Hkv, P, d = stream.k_pre.shape
+    C, Pp = L // page, -(-P // page)
+    scale = 1.0 / math.sqrt(d)
+    res = []
+    for b in range(B):
+        for kv in range(Hkv):
+            pages = [dict(pos=list(range(p * page + 1, min(p * page + page, P) + 1)), ts=0,
+                          pinned=True, slot=p) for p in range(Pp)]
+            per_step = []
+            for i in range(stream.T):
+                t = P + i + 1
+                cur = max(pages, key=lambda pg: pg["pos"][-1]) if pages else None
+                if cur is not None and len(cur["pos"]) < page:
+                    tgt = cur
+                elif len(pages) < C:
+                    tgt = dict(pos=[], ts=0, pinned=False, slot=len(pages))
+                    pages.append(tgt)
+                else:
+                    tgt = min((pg for pg in pages if not pg["pinned"]), key=lambda pg: (pg["ts"], pg["pos"][0]))
+                    tgt.update(pos=[], pinned=False)
+                tgt["pos"].append(t)
+                if not tgt["pinned"]:
+                    tgt["ts"] = t
+                q = bf16_to_f32(stream.q[i, b]).astype(np.float64)
+                allpos = sorted(x for pg in pages for x in pg["pos"])
+                idx = np.array(allpos) - 1
+                probs = []
+                for j in range(g):
+                    e = np.exp(scale * (K[b, kv, idx] @ q[kv * g + j]))
+                    probs.append(dict(zip(allpos, e / e.sum())))
+                dec = [pg for pg in pages if not pg["pinned"]]
+                score = {id(pg): max(pr[x] for pr in probs for x in pg["pos"]) for pg in dec}
+                k = int(np.ceil(np.float32(r) * np.float32(len(dec))))
+                ranked = sorted(dec, key=lambda pg: (-score[id(pg)], pg["pos"][0]))
+                for pg in ranked[:k]:
+                    pg["ts"] = t
+                per_step.append(sorted((pg["slot"], pg["pos"][0], len(pg["pos"]), pg["ts"]) for pg in pages))
+            res.append(per_step)
+    return res
+
+
+@pytest.mark.parametrize("page,L,P,g,r", [(1, 6, 2, 1, 0.5), (2, 8, 2, 2, 0.5), (2, 10, 3, 1, 0.3),
+                                          (1, 7, 1, 3, 0.25)])
+def test_top_r_brute_force(oracle_mod, page, L, P, g, r):
+    B, Hkv, d, T = 2, 2, 4, 10
+    st = gaussian_stream(200 + L + P, B, g * Hkv, Hkv, d, P, T, sigma_q=2.0)
+    ref = brute_force_top_r(st, L, r, page, g)
+    o = oracle_mod.Oracle(L=L, alpha=1e-4, page=page, n_q_heads=g * Hkv, n_kv_heads=Hkv,
+                          head_dim=d, batch=B, stamp_rule=1, top_r=r)
+    o.prefill(st.k_pre, st.v_pre, P)
+    for i in range(T):
+        o.decode_step(st.q[i], st.k[i], st.v[i])
+        state = o.get_state()
+        for u in range(B * Hkv):
+            mine = sorted((p, int(state["start"][u, p]), int(state["count"][u, p]),
+                           int(state["ts"][u, p])) for p in range(L // page) if state["count"][u, p] > 0)
+            assert mine == ref[u][i], (u, i)
