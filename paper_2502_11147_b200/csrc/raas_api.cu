@@ -52,7 +52,7 @@ template <int D>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
-  size_t kvstore, ts, start, cnt, npin, plen, plan, counter, pmax, part_acc, part_ml, status,
+  size_t kvstore, ts, start, cnt, npin, plen, plan, counter, pmax, part_acc, part_ml, status, sched,
       stats, sq, sk, sv, so, total;
 };
 
@@ -113,6 +113,7 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.part_acc = take(U * d.nsplit * g * D * 4);
   L.part_ml = take(U * d.nsplit * g * 8);
   L.status = take(16);
+  L.sched = take(16);
   L.stats = take(64);
   L.sq = take(U * g * D * 2);
   L.sk = take(U * D * 2);
@@ -203,6 +204,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.part_acc = reinterpret_cast<float*>(a + h->lay.part_acc);
   p.part_ml = reinterpret_cast<float2*>(a + h->lay.part_ml);
   p.status = reinterpret_cast<uint32_t*>(a + h->lay.status);
+  p.sched = reinterpret_cast<int32_t*>(a + h->lay.sched);
   p.stats = reinterpret_cast<unsigned long long*>(a + h->lay.stats);
   p.units = h->d.units;
   p.C = h->d.C;

@@ -57,23 +57,33 @@ constexpr int FLAG_END = 4;    // no more work
 constexpr int FLAG_SKIP = 8;   // padding position (keeps every tile aligned to the NC consumers)
 constexpr int CQ_OWNED = 1 << 30;  // combine-queue tag: all splits were processed by this CTA
 
-// Static, batch-size-independent tile schedule of one CTA.  With G CTAs, CTA b owns the whole
-// units [b*fu, (b+1)*fu), fu = units / G, and their splits are combined inside the CTA; the
-// R = units - fu*G remaining units are "shared": their split tiles are dealt round-robin to all
-// CTAs and processed FIRST, so their cross-CTA combines overlap the streaming of owned units and
-// the end of the kernel only waits for CTA-local combines.
+// Tile schedule of one CTA (it never changes numerics: the split arithmetic is schedule-free).
+// With G CTAs, CTA b first streams the whole units [b*fu, (b+1)*fu), fu = units / G, whose
+// splits are combined inside the CTA; then the split tiles of the R = units - fu*G remaining
+// ("shared") units are grabbed dynamically from a global counter, so CTAs that streamed
+// faster take more of them and the kernel ends balanced.  The last CTA to exit resets the
+// counter for the next launch.
 struct TileSched {
-  int b, G, fu, nsplit, n_shared, n_total, shared_base;
+  int b, G, fu, nsplit, n_owned, n_shared_tiles, shared_base, i_owned;
   __device__ TileSched(int units, int nsplit_, int G_, int b_) : b(b_), G(G_), nsplit(nsplit_) {
     fu = units / G;
-    const int RT = (units - fu * G) * nsplit;
-    n_shared = b < RT ? (RT - 1 - b) / G + 1 : 0;
-    n_total = n_shared + fu * nsplit;
+    n_owned = fu * nsplit;
+    n_shared_tiles = (units - fu * G) * nsplit;
     shared_base = fu * G * nsplit;
+    i_owned = 0;
   }
-  __device__ int tile(int i, bool& owned) const {
-    owned = i >= n_shared;
-    return owned ? b * fu * nsplit + (i - n_shared) : shared_base + b + i * G;
+  // next tile for this CTA (warp-uniform), -1 when none is left
+  __device__ int next(int* grab, int lane, bool& owned) {
+    if (i_owned < n_owned) {
+      owned = true;
+      return b * n_owned + i_owned++;
+    }
+    owned = false;
+    if (n_shared_tiles == 0) return -1;
+    int x = 0;
+    if (lane == 0) x = atomicAdd(grab, 1);
+    x = __shfl_sync(0xffffffffu, x, 0);
+    return x < n_shared_tiles ? shared_base + x : -1;
   }
 };
 
@@ -488,19 +498,22 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         ncnt = (lane < SP && q0 + lane < C) ? p.cnt[(size_t)u * C + q0 + lane] : 0;
       }
     };
-    const TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
-    bool owned_next = false;
-    fetch(sched.n_total > 0 ? sched.tile(0, owned_next) : n_tiles);
+    TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
+    bool owned = false, owned_next = false;
+    int tile = sched.next(p.sched, lane, owned);
+    if (tile >= 0) fetch(tile);
     uint32_t j = 0;
     int k = 0;
-    for (int ti = 0; ti < sched.n_total; ++ti) {
-      bool owned;
-      const int tile = sched.tile(ti, owned);
+    while (tile >= 0) {
       const int unit = tile / p.nsplit, split = tile - unit * p.nsplit;
       const int4 pl = nplan;
       const int cntv = ncnt;
-      // next tile's metadata, in flight while this tile is issued
-      fetch(ti + 1 < sched.n_total ? sched.tile(ti + 1, owned_next) : n_tiles);
+      // next tile (and its metadata, in flight while this tile is issued)
+      const int tile_next = sched.next(p.sched, lane, owned_next);
+      if (tile_next >= 0) fetch(tile_next);
+      const bool owned_cur = owned;
+      tile = tile_next;  // loop-carried; the body below uses unit/split/owned_cur
+      owned = owned_next;
       const int used_eff = pl.z, p0 = split * SP;
       const int n = min(p0 + SP, used_eff) - p0;
       if (n <= 0) continue;  // pages not yet allocated (fill phase)
@@ -520,7 +533,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       RAAS_TIMED(0, mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1));  // tile k-2 merged: slots free
       if (lane == 0) {
         tinfo[2 * par] = make_int4(unit, split, (used_eff + SP - 1) / SP, n);
-        tinfo[2 * par + 1] = make_int4((int)j, 0, owned ? 1 : 0, 0);
+        tinfo[2 * par + 1] = make_int4((int)j, 0, owned_cur ? 1 : 0, 0);
         mbar_arrive_expect_tx(qfull(par), g * D * 2);
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
         if (n < NC) mbar_arrive_cnt(mfull(par), (NC - n) * 32);  // warps with no page here
@@ -739,6 +752,26 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           else        mma_bf16_16816(c0, a, qb[ks][0], qb[ks][1]);
         }
       }
+      // V^T fragments now, so the stage can be handed back to the producer before the softmax
+      // and PV math: the ring slot is held ~100 cycles instead of a whole page's compute
+      uint32_t va[KS][4];
+      {
+        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * ROW;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          const int chunk = 2 * mt + (mi & 1);
+          ldsm_x4_t(vrow + ((chunk ^ ri) << 4), va[mt]);
+        }
+      }
+      auto release_stage = [&]() {
+        uint32_t dep = 0;  // consume every fragment: the ldmatrix reads have completed
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) dep ^= va[mt][0] ^ va[mt][1] ^ va[mt][2] ^ va[mt][3];
+        asm volatile("" ::"r"(dep));
+        __syncwarp();
+        mbar_arrive(empty(s));  // stage free for the producer
+      };
+      if (p.score_mode == 0) release_stage();
       float s0 = (c0[0] + c1[0]) * p.scale_log2, s1 = (c0[1] + c1[1]) * p.scale_log2;
       float s2 = (c0[2] + c1[2]) * p.scale_log2, s3 = (c0[3] + c1[3]) * p.scale_log2;
       if (r >= cnt) s0 = s1 = -INFINITY;
@@ -773,6 +806,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
             asm("max.bf16x2 %0, %0, %1;" : "+r"(mxp[i]) : "r"(w[i]));
           }
         }
+        release_stage();  // the page's rows are no longer needed
         float mnv[CQL], mxv[CQL];
 #pragma unroll
         for (int i = 0; i < CQL; ++i) {
@@ -846,18 +880,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       // P^T as the B operand of O^T = V^T P^T: transpose the two 8x8 bf16 blocks in registers
       const uint32_t b0 = movmatrix_t(pack_bf16x2(p0, p1));
       const uint32_t b1 = movmatrix_t(pack_bf16x2(p2, p3));
-      {
-        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * ROW;
 #pragma unroll
-        for (int mt = 0; mt < KS; ++mt) {
-          uint32_t a[4];
-          const int chunk = 2 * mt + (mi & 1);
-          ldsm_x4_t(vrow + ((chunk ^ ri) << 4), a);
-          mma_bf16_16816(acc[mt], a, b0, b1);
-        }
-      }
-      __syncwarp();
-      mbar_arrive(empty(s));  // stage free for the producer
+      for (int mt = 0; mt < KS; ++mt) mma_bf16_16816(acc[mt], va[mt], b0, b1);
 
       if (flags & FLAG_LAST) {  // deposit this warp's softmax state for the tile merge
 #pragma unroll
@@ -879,6 +903,16 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       }
     }
     dbg_add(11, t_start);
+  }
+  // the last CTA out resets the dynamic-schedule counter for the next launch (which reads it
+  // only after griddepcontrol.wait, i.e. after this grid has completed)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int done = atomicAdd(p.sched + 1, 1);
+    if (done == (int)gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+    }
   }
 }
 

@@ -39,6 +39,7 @@ struct DecodeParams {
   const int32_t* npin;
   int4* plan;
   int32_t* counter;
+  int32_t* sched;              // [2]: dynamic tile grab counter, CTA exit counter
   float* pmax;
   float* part_acc;
   float2* part_ml;

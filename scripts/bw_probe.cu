@@ -129,5 +129,26 @@ int main() {
       if (mode != 1) break;
     }
   }
+  // launch-granular streaming: back-to-back launches over distinct 537 MB slices (the size of
+  // one config-3 layer-step), the ceiling for a kernel that must stream that much per launch
+  {
+    const size_t slice = 537ull << 20, nsl = bytes / slice;
+    const int ch = 8192, S = 16;
+    const int smem = S * ch + 2 * S * 8 + 64;
+    auto k = ring_stream<8>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      const int N = 60;
+      for (int i = 0; i < N; ++i)
+        k<<<sms, 9 * 32, smem>>>(a + (i % nsl) * slice, slice / ch, ch, S, 0, 32);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("ring 8K S=16, 537 MB per launch, back-to-back: %.1f us/launch, %.0f GB/s\n",
+             ms / N * 1e3, slice / (ms / N * 1e-3) / 1e9);
+    }
+  }
   return 0;
 }
