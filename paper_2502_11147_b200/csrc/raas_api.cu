@@ -82,6 +82,7 @@ int derive(const raas_config* c, Derived* d) {
   if (c->stamp_rule == 1 && d->C > 512)
     return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports L <= 8192 (512 pages)");
   d->units = c->batch * c->n_kv_heads;
+  if (d->units >= (1 << 20)) return fail(RAAS_E_UNSUPPORTED, "more than 2^20 units per handle");
   if ((long long)d->units * d->C * raas::PAGE >= (1LL << 31))
     return fail(RAAS_E_UNSUPPORTED, "units * L too large for 32-bit TMA row coordinates");
   // auto: 32-page splits (the whole budget when L <= 512); depends on L only, never on batch

@@ -56,6 +56,7 @@ constexpr int FLAG_LAST = 2;   // last page of this tile for the consuming warp
 constexpr int FLAG_END = 4;    // no more work
 constexpr int FLAG_SKIP = 8;   // padding position (keeps every tile aligned to the NC consumers)
 constexpr int CQ_OWNED = 1 << 30;  // combine-queue tag: all splits were processed by this CTA
+constexpr int CQ_UNIT_BITS = 20;   // entry = unit | nse << 20 | owned << 30
 
 // Tile schedule of one CTA (it never changes numerics: the split arithmetic is schedule-free).
 // With G CTAs, CTA b first streams the whole units [b*fu, (b+1)*fu), fu = units / G, whose
@@ -167,47 +168,74 @@ struct DecodeLayout {
 // a5-a7 for one unit, by one warp, after all its splits have published their partials.
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, uint32_t scr,
+__device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, int nse, uint32_t scr,
                                              int lane) {
-  // Latency-oriented: every phase issues all of its global loads before using any of them, so
-  // a unit costs ~3 dependent L2 round trips (ml; acc + page metadata; stores).
-  const int C = p.C, g = p.g, SP = p.split_pages;
-  const int4 pl = __ldcg(p.plan + unit);
-  const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
-  const int used_eff = pl.z, t = pl.w;
-  const int npin = __ldg(p.npin + unit);
-  const int nse = (used_eff + SP - 1) / SP;
+  // Latency-oriented: the plan, the split statistics, the first block of split partials and
+  // the first 128 pages' metadata are all requested before any of them is used (nse comes with
+  // the queue entry), so a unit costs ~one dependent L2 round trip before its stores.
+  const int C = p.C, g = p.g;
   const int NE = nse * g;
   const uint32_t scr_w = scr;                                   // float[nse][g] split weights
   const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
   const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
   const float2* ml_g = p.part_ml + (size_t)unit * p.nsplit * g;
-  // ---- a5 (1): split maxima and sums -> per-head LSE and split weights ----
-  for (int i0 = 0; i0 < NE; i0 += 64) {
-    const int ia = i0 + lane, ib = i0 + 32 + lane;
-    const float2 mla = ia < NE ? __ldcg(ml_g + ia) : make_float2(-INFINITY, 0.f);
-    const float2 mlb = ib < NE ? __ldcg(ml_g + ib) : make_float2(-INFINITY, 0.f);
-    if (ia < NE) { sts_f32(scr_w + 8 * ia, mla.x); sts_f32(scr_w + 8 * ia + 4, mla.y); }
-    if (ib < NE) { sts_f32(scr_w + 8 * ib, mlb.x); sts_f32(scr_w + 8 * ib + 4, mlb.y); }
+  const int4 pl = __ldcg(p.plan + unit);
+  const int npin = __ldg(p.npin + unit);
+  float2 mla[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = 32 * k + lane;
+    mla[k] = i < NE ? __ldcg(ml_g + i) : make_float2(-INFINITY, 0.f);
   }
-  // page metadata for a6/a7, loaded while the split statistics are in flight
+  // page metadata for a6/a7 (bounded by C, masked by the plan's page count later)
   constexpr int PPL = 4;  // pages per lane per chunk
   int tsv[PPL], stv[PPL];
   float pmv[PPL][MAX_GROUP];
-  auto load_meta = [&](int pc) {
+  auto load_meta = [&](int pc, int lim) {
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
       const int pg = pc + 32 * i + lane;
-      const bool ok = pg < used_eff;
+      const bool ok = pg < lim;
       const size_t ix = (size_t)unit * C + pg;
       tsv[i] = ok ? __ldcg(p.ts + ix) : 0;
       stv[i] = ok ? __ldcg(p.start + ix) : 0;
 #pragma unroll
       for (int h = 0; h < MAX_GROUP; ++h)
-        pmv[i][h] = (ok && h < g && pg >= npin) ? __ldcg(p.pmax + ix * g + h) : -INFINITY;
+        pmv[i][h] = (ok && h < g) ? __ldcg(p.pmax + ix * g + h) : -INFINITY;
     }
   };
-  load_meta(0);
+  load_meta(0, C);
+  // first block of split partials: 4 float4 chunks per lane x 2 splits
+  constexpr int CPH = D / 4;                   // chunks per head
+  constexpr int CB = 4, SG = 2;
+  const int nch = g * CPH;
+  const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
+  float4 v[CB][SG];
+  auto load_acc = [&](int cb, int s0) {
+#pragma unroll
+    for (int i = 0; i < CB; ++i) {
+      const int c = lane + 32 * (cb + i), h = c / CPH, d4 = c - h * CPH;
+#pragma unroll
+      for (int u = 0; u < SG; ++u)
+        v[i][u] = (c < nch && s0 + u < nse)
+                      ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  load_acc(0, 0);
+  // ---- a5 (1): split maxima and sums -> per-head LSE and split weights ----
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = 32 * k + lane;
+    if (i < NE) { sts_f32(scr_w + 8 * i, mla[k].x); sts_f32(scr_w + 8 * i + 4, mla[k].y); }
+  }
+  for (int i = 64 + lane; i < NE; i += 32) {  // more than 64 (split, head) pairs
+    const float2 ml = __ldcg(ml_g + i);
+    sts_f32(scr_w + 8 * i, ml.x);
+    sts_f32(scr_w + 8 * i + 4, ml.y);
+  }
+  const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
+  const int used_eff = pl.z, t = pl.w;
   __syncwarp();
   if (lane < g) {  // LSE_h = M + log2 sum_s 2^(m_s - M) l_s   (log2 domain)
     float M = -INFINITY;
@@ -223,27 +251,13 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
     sts_f32(scr_inv + 4 * lane, 1.f / L);
   }
   __syncwarp();
-  // ---- a5 (2): out[h][d] = sum_s w_s acc_s[h][d] / L_h, float4 chunks ----
-  // blocks of 4 chunks per lane x 4 splits: 16 independent 16-byte loads in flight per lane
-  constexpr int CPH = D / 4;                   // chunks per head
-  constexpr int CB = 4, SG = 4;
-  const int nch = g * CPH;
-  const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
+  // ---- a5 (2): out[h][d] = sum_s w_s acc_s[h][d] / L_h ----
   for (int cb = 0; 32 * cb < nch; cb += CB) {
     float4 o[CB];
 #pragma unroll
     for (int i = 0; i < CB; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s0 = 0; s0 < nse; s0 += SG) {
-      float4 v[CB][SG];
-#pragma unroll
-      for (int i = 0; i < CB; ++i) {
-        const int c = lane + 32 * (cb + i), h = c / CPH, d4 = c - h * CPH;
-#pragma unroll
-        for (int u = 0; u < SG; ++u)
-          v[i][u] = (c < nch && s0 + u < nse)
-                        ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      if (cb > 0 || s0 > 0) load_acc(cb, s0);
 #pragma unroll
       for (int i = 0; i < CB; ++i) {
         const int c = lane + 32 * (cb + i), h = c / CPH;
@@ -295,7 +309,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
     const uint32_t scr_key = scr, scr_hist = scr + 8 * 512;
     int nd = 0;
     for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
-      if (pc > 0) load_meta(pc);
+      if (pc > 0) load_meta(pc, used_eff);
 #pragma unroll
       for (int i = 0; i < PPL; ++i) {
         const int pg = pc + 32 * i + lane;
@@ -362,12 +376,12 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, ui
     } else {
       kth = ~0ull;  // nothing stamped
     }
-    if (used_eff > 32 * PPL) load_meta(0);
+    if (used_eff > 32 * PPL) load_meta(0, used_eff);
   }
   Cand best{~0ull, -1};
   int n_stamp = 0, n_dec = 0;
   for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
-    if (pc > 0) load_meta(pc);
+    if (pc > 0) load_meta(pc, used_eff);
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
       const int pg = pc + 32 * i + lane;
@@ -473,12 +487,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       entry = __shfl_sync(0xffffffffu, entry, 0);
       if (lane == 0) mbar_arrive(cqempty(q));  // the entry is read: the slot may be refilled
       if (entry < 0) break;
-      const int unit = entry & (CQ_OWNED - 1);
-      if (!(entry & CQ_OWNED)) fence_acq_rel_gpu();  // partials from other SMs (acquired by merge)
+      const int unit = entry & ((1 << CQ_UNIT_BITS) - 1);
+      const int nse_u = (entry >> CQ_UNIT_BITS) & ((CQ_OWNED >> CQ_UNIT_BITS) - 1);
+      // partials of other SMs: released by their merge warps' acq_rel counter increments and
+      // acquired by ours before the push (CTA-scope handoff to us); read with ld.global.cg
+      if (!(entry & CQ_OWNED)) fence_acq_rel_gpu();
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
-      combine_unit<D>(p, unit, scratch, lane);
+      combine_unit<D>(p, unit, nse_u, scratch, lane);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -590,7 +607,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     int npush = 0;
     auto push = [&](int unit) {  // hand a finished unit (or -1 = END) to the combine warp
 #ifdef RAAS_DBG_TIMING
-      if (lane == 0 && unit >= 0 && (unit & (CQ_OWNED - 1)) < 4096) g_raas_dbg_unit[unit & (CQ_OWNED - 1)][1] = dbg_gtimer();
+      if (lane == 0 && unit >= 0 && (unit & ((1 << CQ_UNIT_BITS) - 1)) < 4096) g_raas_dbg_unit[unit & ((1 << CQ_UNIT_BITS) - 1)][1] = dbg_gtimer();
 #endif
       const int q = npush % CQ;
       RAAS_TIMED(7, mbar_wait(cqempty(q), ((npush / CQ) & 1) ^ 1));
@@ -651,12 +668,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       }
       __syncwarp();
       if (owned) {  // every split of the unit is ours and in order: no cross-CTA counter
-        if (split == nse - 1) push(unit | CQ_OWNED);
+        if (split == nse - 1) push(unit | nse << CQ_UNIT_BITS | CQ_OWNED);
       } else {
         int old = 0;  // release our partial / acquire the others' (gpu scope, cumulative)
         if (lane == 0) old = atom_add_acq_rel_gpu(p.counter + unit, 1);
         old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == nse - 1) push(unit);  // this was the unit's last split
+        if (old == nse - 1) push(unit | nse << CQ_UNIT_BITS);  // the unit's last split
       }
     }
     dbg_add(9, t_start);
