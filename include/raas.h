@@ -85,6 +85,16 @@ typedef struct {
                                 unpinned resident pages, ties to the oldest page (reading D23).
                                 Needs L <= 8192. */
   float   top_r;         /* r in [0, 1] for stamp_rule 1 (0.5 in the paper) */
+  int32_t quest_prefill_pages; /* 0 = off.  K > 0: the Quest-on-prefill + RaaS-on-decode hybrid
+                            the paper recommends for long prompts / small budgets (:173, :183,
+                            :237; reading D24).  Each step a unit attends only the K full prompt
+                            pages with the largest representative-key bound
+                            max_h sum_c max(q_c min_c, q_c max_c) (ties: lower page), plus all
+                            other resident pages; stamping / eviction are unchanged (prompt pages
+                            stay pinned and resident).  Adds two small launches per step
+                            (bound, selection) and 1/16 of the prompt's K bytes.  L <= 8192.
+                            With raas_set_state, every pinned page is treated as a full prompt
+                            page. */
 } raas_config;
 
 /* Bytes of device memory the handle needs (KV store: per unit L/16 pages, each 16 K rows + 16 V

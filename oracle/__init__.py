@@ -50,6 +50,7 @@ class _Cfg(ctypes.Structure):
         ("score_mode", ctypes.c_int32),
         ("stamp_rule", ctypes.c_int32),
         ("top_r", ctypes.c_double),
+        ("quest_prefill_pages", ctypes.c_int32),
     ]
 
 
@@ -72,6 +73,7 @@ def lib():
         l.raas_ref_set_state.argtypes = [P, P, P, P, P, P, P, P]
         l.raas_ref_get_trace.argtypes = [P, P, P, P]
         l.raas_ref_resident_positions.argtypes = [P, ctypes.c_int32, P, ctypes.c_int32]
+        l.raas_ref_get_selection.argtypes = [P, P, P]
         l.raas_ref_set_threads.argtypes = [ctypes.c_int]
         _lib = l
     return _lib
@@ -95,9 +97,10 @@ class Oracle:
     """fp64 RaaS state machine over `batch * n_kv_heads` independent units (host)."""
 
     def __init__(self, L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch,
-                 softmax_scale=0.0, score_mode=0, stamp_rule=0, top_r=0.5):
+                 softmax_scale=0.0, score_mode=0, stamp_rule=0, top_r=0.5,
+                 quest_prefill_pages=0):
         self.cfg = _Cfg(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
-                        score_mode, stamp_rule, top_r)
+                        score_mode, stamp_rule, top_r, quest_prefill_pages)
         self.C = L // page if page > 0 else 0
         self.units = batch * n_kv_heads
         self.page, self.d, self.hq, self.hkv, self.batch = page, head_dim, n_q_heads, n_kv_heads, batch
@@ -178,6 +181,13 @@ class Oracle:
         ps = np.zeros((U, C), np.float64)
         lib().raas_ref_get_trace(self._h, _ptr(ev), _ptr(sl), _ptr(ps))
         return dict(evicted=ev, slot=sl, pstar=ps)
+
+    def get_selection(self):
+        U, C = self.units, self.C
+        att = np.zeros((U, C), np.uint8)
+        qs = np.zeros((U, C), np.float64)
+        lib().raas_ref_get_selection(self._h, _ptr(att), _ptr(qs))
+        return dict(attended=att, qscore=qs)
 
     def resident_positions(self, unit):
         cap = self.C * self.page

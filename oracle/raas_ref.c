@@ -36,6 +36,9 @@ typedef struct {
   int32_t used, cur, t;
   int32_t evicted, slot;  /* trace of the last step */
   double *pstar;          /* [C] */
+  int32_t nfull;          /* full prompt pages (selectable in the hybrid mode) */
+  uint8_t *attended;      /* [C] hybrid trace */
+  double *qscore;         /* [C] hybrid trace */
 } ref_unit;
 
 struct raas_ref {
@@ -77,6 +80,7 @@ int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
   if (cfg->score_mode != 0 && cfg->score_mode != 1) return REF_E_INVALID;
   if (cfg->stamp_rule != 0 && cfg->stamp_rule != 1) return REF_E_INVALID;
   if (cfg->stamp_rule == 1 && !(cfg->top_r >= 0.0 && cfg->top_r <= 1.0)) return REF_E_INVALID;
+  if (cfg->quest_prefill_pages < 0) return REF_E_INVALID;
   raas_ref* h = (raas_ref*)calloc(1, sizeof *h);
   if (!h) return REF_E_INVALID;
   h->cfg = *cfg;
@@ -93,6 +97,8 @@ int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
     u->ts = (int32_t*)calloc((size_t)h->C, sizeof(int32_t));
     u->pinned = (uint8_t*)calloc((size_t)h->C, 1);
     u->pstar = (double*)calloc((size_t)h->C, sizeof(double));
+    u->attended = (uint8_t*)calloc((size_t)h->C, 1);
+    u->qscore = (double*)calloc((size_t)h->C, sizeof(double));
     u->K = (double*)calloc(kv, sizeof(double));
     u->V = (double*)calloc(kv, sizeof(double));
     u->cur = -1;
@@ -108,7 +114,7 @@ void raas_ref_destroy(raas_ref* h) {
   for (int32_t i = 0; i < h->units; ++i) {
     ref_unit* u = &h->u[i];
     free(u->start); free(u->count); free(u->ts); free(u->pinned);
-    free(u->pstar); free(u->K); free(u->V);
+    free(u->pstar); free(u->K); free(u->V); free(u->attended); free(u->qscore);
   }
   free(h->u);
   free(h);
@@ -146,6 +152,7 @@ int raas_ref_prefill_varlen(raas_ref* h, const uint16_t* k, const uint16_t* v, c
     u->used = Pp;
     u->cur = Pp - 1;                              /* -1 when P == 0 */
     u->t = Pu;
+    u->nfull = Pu / page;
     u->evicted = -1;
     u->slot = -1;
   }
@@ -218,13 +225,51 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
   double* qh = (double*)malloc((size_t)d * sizeof(double));
   for (int32_t p = 0; p < C; ++p) best[p] = -INFINITY;
 
+  /* which pages this step attends: all resident pages, except that the hybrid mode keeps only
+   * the K best full prompt pages by Quest's representative-key bound (D24) */
+  const int32_t Kq = h->cfg.quest_prefill_pages;
+  for (int32_t p = 0; p < C; ++p) {
+    u->attended[p] = u->count[p] > 0;
+    u->qscore[p] = -INFINITY;
+  }
+  if (Kq > 0 && u->nfull > Kq) {
+    for (int32_t p = 0; p < u->nfull; ++p) {
+      double sc = -INFINITY;
+      for (int32_t hh = 0; hh < g; ++hh) {
+        const int32_t qi = b * Hq + kvh * g + hh;
+        double U = 0.0;
+        for (int32_t c = 0; c < d; ++c) {
+          double mn = INFINITY, mxk = -INFINITY;
+          for (int32_t i = 0; i < u->count[p]; ++i) {
+            const double kc = u->K[((size_t)p * page + i) * d + c];
+            if (kc < mn) mn = kc;
+            if (kc > mxk) mxk = kc;
+          }
+          const double qc = widen_bf16(q[(size_t)qi * d + c]);
+          U += (qc * mn > qc * mxk) ? qc * mn : qc * mxk;
+        }
+        if (U > sc) sc = U;
+      }
+      u->qscore[p] = sc;
+      u->attended[p] = 0;
+    }
+    for (int32_t r = 0; r < Kq; ++r) {            /* top-K by (score desc, page asc) */
+      int32_t arg = -1;
+      for (int32_t p = 0; p < u->nfull; ++p) {
+        if (u->attended[p]) continue;
+        if (arg < 0 || u->qscore[p] > u->qscore[arg]) arg = p;
+      }
+      u->attended[arg] = 1;
+    }
+  }
+
   for (int32_t hh = 0; hh < g; ++hh) {            /* q-head h uses kv-head floor(h/g) (D15) */
     const int32_t qi = b * Hq + kvh * g + hh;
     for (int32_t c = 0; c < d; ++c) qh[c] = widen_bf16(q[(size_t)qi * d + c]);
     /* scores s_j = scale * <q, k_j> over every resident token (D2, D20) */
     double mx = -INFINITY;
     for (int32_t p = 0; p < C; ++p)
-      for (int32_t i = 0; i < u->count[p]; ++i) {
+      for (int32_t i = 0; i < (u->attended[p] ? u->count[p] : 0); ++i) {
         const double* kj = &u->K[((size_t)p * page + i) * d];
         double acc = 0.0;
         for (int32_t c = 0; c < d; ++c) acc += qh[c] * kj[c];
@@ -234,13 +279,13 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
     /* LSE = log sum_j exp(s_j)  (softmax normaliser, :70) */
     double sum = 0.0;
     for (int32_t p = 0; p < C; ++p)
-      for (int32_t i = 0; i < u->count[p]; ++i) sum += exp(s[p * page + i] - mx);
+      for (int32_t i = 0; i < (u->attended[p] ? u->count[p] : 0); ++i) sum += exp(s[p * page + i] - mx);
     const double lse = mx + log(sum);
     if (out) {
       double* o = out + (size_t)qi * d;
       for (int32_t c = 0; c < d; ++c) o[c] = 0.0;
       for (int32_t p = 0; p < C; ++p)
-        for (int32_t i = 0; i < u->count[p]; ++i) {
+        for (int32_t i = 0; i < (u->attended[p] ? u->count[p] : 0); ++i) {
           const double w = exp(s[p * page + i] - lse);
           const double* vj = &u->V[((size_t)p * page + i) * d];
           for (int32_t c = 0; c < d; ++c) o[c] += w * vj[c];
@@ -370,6 +415,9 @@ int raas_ref_set_state(raas_ref* h, const int32_t* t, const int32_t* ts,
     memcpy(u->pinned, pinned + (size_t)ui * C, (size_t)C);
     u->used = 0;
     u->cur = -1;
+    u->nfull = 0;
+    for (int32_t p = 0; p < C; ++p)
+      if (u->pinned[p]) u->nfull += 1;            /* set_state: pinned pages are full prompt pages */
     for (int32_t p = 0; p < C; ++p) {
       if (u->count[p] > 0) {
         u->used += 1;
@@ -394,6 +442,15 @@ int raas_ref_get_trace(const raas_ref* h, int32_t* evicted, int32_t* slot, doubl
     if (evicted) evicted[ui] = u->evicted;
     if (slot) slot[ui] = u->slot;
     if (pstar) memcpy(pstar + (size_t)ui * h->C, u->pstar, (size_t)h->C * sizeof(double));
+  }
+  return REF_OK;
+}
+
+int raas_ref_get_selection(const raas_ref* h, uint8_t* attended, double* qscore) {
+  if (!h) return REF_E_INVALID;
+  for (int32_t ui = 0; ui < h->units; ++ui) {
+    if (attended) memcpy(attended + (size_t)ui * h->C, h->u[ui].attended, (size_t)h->C);
+    if (qscore) memcpy(qscore + (size_t)ui * h->C, h->u[ui].qscore, (size_t)h->C * sizeof(double));
   }
   return REF_OK;
 }

@@ -47,6 +47,11 @@ typedef struct {
                             the k = ceilf(top_r * n) best-scored of the n unpinned resident pages,
                             ranked by (score desc, start_pos asc) (reading D23) */
   double  top_r;
+  int32_t quest_prefill_pages; /* 0 = off.  K > 0: the Quest-on-prefill + RaaS-on-decode hybrid
+                            (PAPER.md :173/:183, :237; reading D24): each step a unit attends
+                            only the K full prompt pages with the largest representative-key
+                            bound max_h sum_c max(q_hc min_c, q_hc max_c) (ties: lower page), plus
+                            every other resident page; the prompt's KV stays resident */
 } raas_ref_config;
 
 typedef struct raas_ref raas_ref;
@@ -81,6 +86,10 @@ int  raas_ref_set_state(raas_ref* h, const int32_t* t, const int32_t* ts,
  *   pstar[unit*C+p]= max_{h in group, j in p} p_{h,j} for unpinned resident pages,
  *                    -1 otherwise (used for the |p*-alpha| exactness band) */
 int  raas_ref_get_trace(const raas_ref* h, int32_t* evicted, int32_t* slot, double* pstar);
+/* hybrid mode trace of the last step: attended[unit*C+p] (1 if page p was attended) and
+ * qscore[unit*C+p] (the selection score of full prompt pages, -inf otherwise); either may be
+ * NULL */
+int  raas_ref_get_selection(const raas_ref* h, uint8_t* attended, double* qscore);
 /* resident token positions of one unit after the last step, ascending; returns count */
 int  raas_ref_resident_positions(const raas_ref* h, int32_t unit, int32_t* pos, int32_t cap);
 /* threads used by the OpenMP loop over units (1 = serial); returns the effective count */

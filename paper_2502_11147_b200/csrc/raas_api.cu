@@ -52,7 +52,7 @@ template <int D>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
-  size_t kvstore, ts, start, cnt, npin, plen, plan, counter, pmax, part_acc, part_ml, status, sched,
+  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, qscore, vmap, counter, pmax, part_acc, part_ml, status, sched,
       stats, sq, sk, sv, so, total;
 };
 
@@ -81,6 +81,9 @@ int derive(const raas_config* c, Derived* d) {
   d->C = c->L / c->page;
   if (c->stamp_rule == 1 && d->C > 512)
     return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports L <= 8192 (512 pages)");
+  if (c->quest_prefill_pages < 0) return fail(RAAS_E_INVALID, "quest_prefill_pages must be >= 0");
+  if (c->quest_prefill_pages > 0 && d->C > 512)
+    return fail(RAAS_E_UNSUPPORTED, "the Quest-on-prefill hybrid supports L <= 8192 (512 pages)");
   d->units = c->batch * c->n_kv_heads;
   if (d->units >= (1 << 20)) return fail(RAAS_E_UNSUPPORTED, "more than 2^20 units per handle");
   if ((long long)d->units * d->C * raas::PAGE >= (1LL << 31))
@@ -107,6 +110,11 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.start = take(U * C * 4);
   L.cnt = take(U * C * 4);
   L.npin = take(U * 4);
+  L.nfull = take(U * 4);
+  const bool hyb = c->quest_prefill_pages > 0;  // Quest-on-prefill hybrid workspace (NEXT-4)
+  L.repkey = hyb ? take(U * C * 2 * D * 2) : 0;
+  L.qscore = hyb ? take(U * C * 4) : 0;
+  L.vmap = hyb ? take(U * C * 4) : 0;
   L.plen = take((size_t)c->batch * 4);
   L.plan = take(U * 16);
   L.counter = take(U * 4);
@@ -215,11 +223,28 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.score_mode = h->cfg.score_mode;
   p.stamp_rule = h->cfg.stamp_rule;
   p.top_r = h->cfg.top_r;
+  p.quest_k = h->cfg.quest_prefill_pages;
+  p.nfull = reinterpret_cast<const int32_t*>(a + h->lay.nfull);
+  p.vmap = h->cfg.quest_prefill_pages > 0 ? reinterpret_cast<const int32_t*>(a + h->lay.vmap) : nullptr;
   const float scale = h->cfg.softmax_scale > 0.f ? h->cfg.softmax_scale
                                                  : 1.0f / sqrtf((float)h->cfg.head_dim);
   p.scale_log2 = scale * 1.4426950408889634f;
   p.log2_alpha = h->cfg.alpha > 0.f ? log2f(h->cfg.alpha) : -INFINITY;
 
+  if (p.quest_k > 0) {  // hybrid: this step's prompt-page selection from q (D24)
+    const int units = h->d.units, C = h->d.C;
+    const int chunks = (C + 31) / 32;
+    const long long warps = (long long)units * chunks;
+    raas::raas_qbound_kernel<D><<<(int)((warps + 7) / 8), 256, 0, st>>>(
+        p.q, reinterpret_cast<const __nv_bfloat16*>(a + h->lay.repkey), p.nfull,
+        reinterpret_cast<float*>(a + h->lay.qscore), units, C, p.g, p.quest_k);
+    RAAS_CUDA(cudaGetLastError());
+    const int wpb = 4;
+    raas::raas_qselect_kernel<<<(units + wpb - 1) / wpb, 32 * wpb, wpb * (8 * C + 1024), st>>>(
+        reinterpret_cast<const float*>(a + h->lay.qscore), p.nfull,
+        reinterpret_cast<int32_t*>(a + h->lay.vmap), units, C, p.quest_k);
+    RAAS_CUDA(cudaGetLastError());
+  }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(h->grid);
   lc.blockDim = dim3(Lay<D>::THREADS);
@@ -268,6 +293,22 @@ int setup_kernel(raas_handle* h) {
   RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
   h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
+  return RAAS_OK;
+}
+
+int build_repkeys(raas_handle* h, cudaStream_t st) {
+  if (h->cfg.quest_prefill_pages <= 0) return RAAS_OK;
+  uint8_t* a = h->arena;
+  const size_t total = (size_t)h->d.units * h->d.C * (h->cfg.head_dim / 8);
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)h->num_sms * 16);
+  auto* kvs = reinterpret_cast<const __nv_bfloat16*>(a + h->lay.kvstore);
+  auto* rk = reinterpret_cast<__nv_bfloat16*>(a + h->lay.repkey);
+  auto* nf = reinterpret_cast<const int32_t*>(a + h->lay.nfull);
+  if (h->cfg.head_dim == 128)
+    raas::raas_repkey_kernel<128><<<blocks, 256, 0, st>>>(kvs, rk, nf, h->d.units, h->d.C);
+  else
+    raas::raas_repkey_kernel<64><<<blocks, 256, 0, st>>>(kvs, rk, nf, h->d.units, h->d.C);
+  RAAS_CUDA(cudaGetLastError());
   return RAAS_OK;
 }
 
@@ -379,9 +420,11 @@ int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int3
   raas::raas_meta_init<<<(int)std::min<size_t>((n + 255) / 256, 4096), 256, 0, st>>>(
       reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
       reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
-      reinterpret_cast<int4*>(a + h->lay.plan), plen, h->d.units, h->cfg.n_kv_heads, h->d.C);
+      reinterpret_cast<int32_t*>(a + h->lay.nfull), reinterpret_cast<int4*>(a + h->lay.plan), plen,
+      h->d.units, h->cfg.n_kv_heads, h->d.C);
   RAAS_CUDA(cudaGetLastError());
-  int rc = refresh(h, st);
+  int rc = build_repkeys(h, st);
+  if (!rc) rc = refresh(h, st);
   if (rc) return rc;
   h->prefilled = 1;
   return RAAS_OK;
@@ -486,6 +529,8 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.start, start_pos, U * C * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.cnt, count, U * C * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.npin, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
+  // set_state: the pinned pages are taken as full prompt pages (hybrid selection set)
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.nfull, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.plan, plan.data(), U * 16, cudaMemcpyHostToDevice, st));
   const size_t pages = U * C, D = h->cfg.head_dim;
   std::vector<uint16_t> dev;
@@ -499,7 +544,8 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
                dev.data(), pages, (int)D);
     RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kvstore, dev.data(), dev.size() * 2, cudaMemcpyHostToDevice, st));
   }
-  int rc = refresh(h, st);
+  int rc = build_repkeys(h, st);
+  if (!rc) rc = refresh(h, st);
   if (rc) return rc;
   RAAS_CUDA(cudaStreamSynchronize(st));
   h->prefilled = 1;

@@ -326,53 +326,9 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     krem = krem < 0 ? 0 : (krem > nd ? nd : krem);
     __syncwarp();
     if (krem > 0) {
-      // radix select of the krem-th largest 64-bit key, 8 bits per pass, smem histogram
-      unsigned long long prefix = 0, mask = 0;
-      for (int shift = 56; shift >= 0; shift -= 8) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sts_f32(scr_hist + 4 * (lane * 8 + j), 0.f);
-        __syncwarp();
-        for (int pg = lane; pg < used_eff; pg += 32) {
-          unsigned long long key;
-          asm volatile("ld.shared.u64 %0, [%1];" : "=l"(key) : "r"(scr_key + 8 * pg));
-          if (key != 0 && (key & mask) == prefix)
-            atomicAdd(reinterpret_cast<int*>(__cvta_shared_to_generic(scr_hist)) +
-                          ((key >> shift) & 255), 1);
-        }
-        __syncwarp();
-        // bins in descending digit order: lane l owns digits 255-8l .. 248-8l
-        int c[8], tot = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          c[j] = __float_as_int(lds_f32(scr_hist + 4 * (255 - (lane * 8 + j))));
-          tot += c[j];
-        }
-        int incl = tot;  // inclusive prefix over lanes (higher digits first)
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const int excl = incl - tot;
-        const unsigned hit = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
-        const int src = __ffs(hit) - 1;
-        int digit = 0, above = 0;
-        if (lane == src) {
-          int run = excl;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (run + c[j] >= krem) { digit = 255 - (lane * 8 + j); above = run; break; }
-            run += c[j];
-          }
-        }
-        digit = __shfl_sync(0xffffffffu, digit, src);
-        above = __shfl_sync(0xffffffffu, above, src);
-        krem -= above;
-        prefix |= static_cast<unsigned long long>(digit) << shift;
-        mask |= 255ull << shift;
-        __syncwarp();
-      }
-      kth = prefix;  // keys are unique (start positions differ): exactly k keys are >= kth
+      // keys are unique (start positions differ): exactly k keys are >= kth
+      kth = warp_kth_largest(scr_key, scr_hist, used_eff, krem, lane);
+
     } else {
       kth = ~0ull;  // nothing stamped
     }
@@ -508,11 +464,20 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     const uint64_t pol = l2_evict_first_policy();
     int4 nplan = make_int4(0, 0, 0, 0);
     int ncnt = 0;
+    // a tile covers the "attended page list" positions v in [split*SP, split*SP + SP): the
+    // resident pages in index order, or, in the Quest-on-prefill hybrid (NEXT-4), the K
+    // selected full prompt pages (from raas_qselect) followed by every page from nfull on
+    int nphys = 0, nnatt = 0;
     auto fetch = [&](int tl) {
       if (tl < n_tiles) {
         const int u = tl / p.nsplit, q0 = (tl - u * p.nsplit) * SP;
         nplan = p.plan[u];
-        ncnt = (lane < SP && q0 + lane < C) ? p.cnt[(size_t)u * C + q0 + lane] : 0;
+        const int nf = p.quest_k > 0 ? p.nfull[u] : 0;
+        const bool hyb = p.quest_k > 0 && nf > p.quest_k;
+        const int v = q0 + lane;
+        nnatt = hyb ? p.quest_k + nplan.z - nf : nplan.z;
+        nphys = !hyb ? v : (v < p.quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - p.quest_k));
+        ncnt = (lane < SP && v < nnatt) ? p.cnt[(size_t)u * C + nphys] : 0;
       }
     };
     TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
@@ -524,15 +489,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     while (tile >= 0) {
       const int unit = tile / p.nsplit, split = tile - unit * p.nsplit;
       const int4 pl = nplan;
-      const int cntv = ncnt;
+      const int cntv = ncnt, physv = nphys, natt = nnatt;
       // next tile (and its metadata, in flight while this tile is issued)
       const int tile_next = sched.next(p.sched, lane, owned_next);
       if (tile_next >= 0) fetch(tile_next);
       const bool owned_cur = owned;
       tile = tile_next;  // loop-carried; the body below uses unit/split/owned_cur
       owned = owned_next;
-      const int used_eff = pl.z, p0 = split * SP;
-      const int n = min(p0 + SP, used_eff) - p0;
+      const int p0 = split * SP;
+      const int n = min(p0 + SP, natt) - p0;
       if (n <= 0) continue;  // pages not yet allocated (fill phase)
       const int slot = pl.x, off = pl.y & 0xffff;
       // align the tile to the consumer count: page i of a tile is always consumed by warp
@@ -549,7 +514,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       const int par = k & 1;
       RAAS_TIMED(0, mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1));  // tile k-2 merged: slots free
       if (lane == 0) {
-        tinfo[2 * par] = make_int4(unit, split, (used_eff + SP - 1) / SP, n);
+        tinfo[2 * par] = make_int4(unit, split, (natt + SP - 1) / SP, n);
         tinfo[2 * par + 1] = make_int4((int)j, 0, owned_cur ? 1 : 0, 0);
         mbar_arrive_expect_tx(qfull(par), g * D * 2);
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
@@ -563,11 +528,11 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       for (int i0 = 0; i0 < n; i0 += BATCH) {
         const int nb = min(BATCH, n - i0);
         const int c = __shfl_sync(0xffffffffu, cntv, (i0 + lane) & 31);
+        const int page = __shfl_sync(0xffffffffu, physv, (i0 + lane) & 31);
         if (lane < nb) {
           const int i = i0 + lane;
           const uint32_t jj = j + lane;
           const int s = (int)(jj % S);
-          const int page = p0 + i;
           RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
           const bool is_slot = page == slot;
           sinfo[2 * s] = make_int4(unit, page, is_slot ? off + 1 : c, is_slot ? off : -1);

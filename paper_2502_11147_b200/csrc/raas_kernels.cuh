@@ -49,6 +49,9 @@ struct DecodeParams {
   int score_mode;    // 0 exact page max (D4), 1 Quest representative-key bound (D22)
   int stamp_rule;    // 0 threshold alpha (D2/D3), 1 top-r fraction of pages (D23)
   float top_r;
+  int quest_k;       // > 0: Quest-on-prefill hybrid (D24), pages selected per step
+  const int32_t* nfull;  // [units] full prompt pages (selectable)
+  const int32_t* vmap;   // [units][C] selected prompt pages of this step, ascending
   float scale_log2;  // softmax_scale * log2(e)
   float log2_alpha;  // log2(alpha); -inf for alpha == 0
 };
@@ -77,6 +80,66 @@ __device__ __forceinline__ int warp_argmin_page(const Cand& c) {
   const unsigned ball = __ballot_sync(0xffffffffu, c.key == m && c.page >= 0);
   if (ball == 0) return -1;
   return __shfl_sync(0xffffffffu, c.page, __ffs(ball) - 1);
+}
+
+// k-th largest (1 <= k <= number of non-zero keys) of the 64-bit keys key[0..n) held in shared
+// memory (zero = not a candidate), by one warp: radix select, 8 bits per pass, with a
+// 256-bin shared histogram at `hist` (1 KiB).  Every lane returns the key.
+__device__ __forceinline__ unsigned long long warp_kth_largest(uint32_t keys, uint32_t hist,
+                                                               int n, int k, int lane) {
+  unsigned long long prefix = 0, mask = 0;
+  int krem = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(hist + 4 * (lane * 8 + j)), "r"(0) : "memory");
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      unsigned long long key;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(key) : "r"(keys + 8 * i));
+      if (key != 0 && (key & mask) == prefix)
+        atomicAdd(reinterpret_cast<int*>(__cvta_shared_to_generic(hist)) + ((key >> shift) & 255), 1);
+    }
+    __syncwarp();
+    int c[8], tot = 0;  // lane l owns digits 255-8l .. 248-8l (descending)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c[j]) : "r"(hist + 4 * (255 - (lane * 8 + j))));
+      tot += c[j];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int excl = incl - tot;
+    const unsigned hit = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
+    const int src = __ffs(hit) - 1;
+    int digit = 0, above = 0;
+    if (lane == src) {
+      int run = excl;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (run + c[j] >= krem) { digit = 255 - (lane * 8 + j); above = run; break; }
+        run += c[j];
+      }
+    }
+    digit = __shfl_sync(0xffffffffu, digit, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    krem -= above;
+    prefix |= static_cast<unsigned long long>(digit) << shift;
+    mask |= 255ull << shift;
+    __syncwarp();
+  }
+  return prefix;
+}
+
+// sortable 64-bit ranking key: larger float first, then smaller tie index; never 0
+__device__ __forceinline__ unsigned long long rank_key(float x, uint32_t tie) {
+  const uint32_t b = __float_as_uint(x);
+  const uint32_t sx = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return (static_cast<unsigned long long>(sx) << 32) | (0xffffffffu - tie);
 }
 
 // plan for the step after one that wrote `off_written` (0-based) into `slot` at time t
@@ -124,8 +187,8 @@ __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
 // metadata after prefill: unit u's pages < Pp(u) pinned and full (the last may be partial),
 // t = P(u), with P(u) = plen[u / n_kv_heads] (variable prompt lengths, NEXT-2)
 __global__ void raas_meta_init(int32_t* ts, int32_t* start, int32_t* cnt, int32_t* npin,
-                               int4* plan, const int32_t* __restrict__ plen, int units,
-                               int n_kv_heads, int C) {
+                               int32_t* nfull, int4* plan, const int32_t* __restrict__ plen,
+                               int units, int n_kv_heads, int C) {
   const size_t total = (size_t)units * C;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -138,6 +201,7 @@ __global__ void raas_meta_init(int32_t* ts, int32_t* start, int32_t* cnt, int32_
     cnt[i] = pg < Pp ? min(PAGE, P - pg * PAGE) : 0;
     if (pg == 0) {
       npin[u] = Pp;
+      nfull[u] = P / PAGE;  // full prompt pages: selectable by the hybrid mode (D24)
       plan[u] = make_int4(0, 0, 0, P + 1);  // .w = t + 1; the rest derived by raas_refresh
     }
   }
@@ -183,6 +247,123 @@ __global__ void raas_refresh(const int32_t* ts, const int32_t* start, const int3
     }
     plan[unit] = pl;
     counter[unit] = 0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Quest-on-prefill + RaaS-on-decode hybrid (SURVEY NEXT-4; PAPER.md :173/:183, :237; D24)
+// ------------------------------------------------------------------------------------------
+// Representative keys of the full prompt pages: per channel min and max over the 16 keys
+// (exact in bf16), repkey [units][C][2][D].
+template <int D>
+__global__ void raas_repkey_kernel(const __nv_bfloat16* __restrict__ kvstore,
+                                   __nv_bfloat16* repkey, const int32_t* __restrict__ nfull,
+                                   int units, int C) {
+  constexpr int NCH = D / 8;
+  const size_t total = (size_t)units * C * NCH;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % NCH);
+    const size_t pu = i / NCH;
+    const int pg = (int)(pu % C);
+    const size_t u = pu / C;
+    if (pg >= nfull[u]) continue;
+    const __nv_bfloat16* kp = kvstore + pu * 2 * PAGE * D;
+    uint32_t mn[4] = {0x7f807f80u, 0x7f807f80u, 0x7f807f80u, 0x7f807f80u};
+    uint32_t mx[4] = {0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u};
+#pragma unroll
+    for (int r = 0; r < PAGE; ++r) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(kp + r * D) + (ch ^ (r & 7)));
+      const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        asm("min.bf16x2 %0, %0, %1;" : "+r"(mn[e]) : "r"(wv[e]));
+        asm("max.bf16x2 %0, %0, %1;" : "+r"(mx[e]) : "r"(wv[e]));
+      }
+    }
+    *reinterpret_cast<uint4*>(repkey + (pu * 2 + 0) * D + ch * 8) = make_uint4(mn[0], mn[1], mn[2], mn[3]);
+    *reinterpret_cast<uint4*>(repkey + (pu * 2 + 1) * D + ch * 8) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
+  }
+}
+
+// Quest bound of every full prompt page: max over the group's heads of
+// sum_c max(q_c min_c, q_c max_c).  One warp per (unit, 32 pages), a lane per page.
+template <int D>
+__global__ void raas_qbound_kernel(const __nv_bfloat16* __restrict__ q,
+                                   const __nv_bfloat16* __restrict__ repkey,
+                                   const int32_t* __restrict__ nfull, float* qscore, int units,
+                                   int C, int g, int K) {
+  const int wid = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int chunks = (C + 31) / 32;
+  const int u = wid / chunks, c0 = (wid - u * chunks) * 32;
+  if (u >= units) return;
+  const int nf = nfull[u];
+  if (nf <= K || c0 >= nf) return;
+  const int pg = c0 + lane;
+  const bool ok = pg < nf;
+  float U[MAX_GROUP];
+#pragma unroll
+  for (int h = 0; h < MAX_GROUP; ++h) U[h] = 0.f;
+  const size_t pu = (size_t)u * C + (ok ? pg : 0);
+  for (int c8 = 0; c8 < D / 8; ++c8) {
+    const uint4 mnv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 0) * D) + c8);
+    const uint4 mxv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 1) * D) + c8);
+    const uint32_t mnw[4] = {mnv.x, mnv.y, mnv.z, mnv.w}, mxw[4] = {mxv.x, mxv.y, mxv.z, mxv.w};
+#pragma unroll
+    for (int h = 0; h < MAX_GROUP; ++h) {
+      if (h < g) {
+        const uint4 qv = __ldg(reinterpret_cast<const uint4*>(q + ((size_t)u * g + h) * D) + c8);
+        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t sh = (e & 1) ? 0u : 16u;
+          const float qf = __uint_as_float((qw[e >> 1] << sh) & 0xffff0000u);
+          const float a = __uint_as_float((mnw[e >> 1] << sh) & 0xffff0000u);
+          const float b = __uint_as_float((mxw[e >> 1] << sh) & 0xffff0000u);
+          U[h] += fmaxf(qf * a, qf * b);
+        }
+      }
+    }
+  }
+  float sc = -INFINITY;
+#pragma unroll
+  for (int h = 0; h < MAX_GROUP; ++h)
+    if (h < g) sc = fmaxf(sc, U[h]);
+  if (ok) qscore[(size_t)u * C + pg] = sc;
+}
+
+// Top-K full prompt pages by (bound desc, page asc) -> vmap[u][0..K) in ascending page order.
+// One warp per unit; shared memory: per warp 8*C bytes of keys + 1 KiB histogram.
+__global__ void raas_qselect_kernel(const float* __restrict__ qscore,
+                                    const int32_t* __restrict__ nfull, int32_t* vmap, int units,
+                                    int C, int K) {
+  extern __shared__ uint8_t qs_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (u >= units) return;
+  const int nf = nfull[u];
+  if (nf <= K) return;
+  const uint32_t keys = smem_u32(qs_smem) + warp * (8 * C + 1024);
+  const uint32_t hist = keys + 8 * C;
+  for (int pg = lane; pg < nf; pg += 32) {
+    const unsigned long long key = rank_key(qscore[(size_t)u * C + pg], (uint32_t)pg);
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys + 8 * pg), "l"(key) : "memory");
+  }
+  __syncwarp();
+  const unsigned long long kth = warp_kth_largest(keys, hist, nf, K, lane);
+  int base = 0;
+  for (int c0 = 0; c0 < nf; c0 += 32) {  // ascending compaction of the selected pages
+    const int pg = c0 + lane;
+    bool sel = false;
+    if (pg < nf) {
+      unsigned long long key;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(key) : "r"(keys + 8 * pg));
+      sel = key >= kth;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, sel);
+    if (sel) vmap[(size_t)u * C + base + __popc(b & ((1u << lane) - 1))] = pg;
+    base += __popc(b);
   }
 }
 

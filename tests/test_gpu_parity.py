@@ -452,3 +452,36 @@ def test_top_r_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, r, score):
     assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
     c = layer.raas_get_counters()
     assert 0 < c["stamps"] < c["decisions"]
+
+
+# ------------------------------------------------------------------ NEXT-4: Quest-on-prefill hybrid
+
+
+def _long_prompt_stream(seed, B, Hq, Hkv, d, P, T):
+    """Long prompt with page-correlated keys (waterfall signatures) so the per-step selection
+    of prompt pages is well separated; a short decode."""
+    return waterfall_stream(seed, B, Hq, Hkv, d, P, T, lam=6.0, p_phoenix=1.0 / 16, phoenix_len=8)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,K,sp", [
+    (2, 8, 2, 128, 512, 200, 768, 6, 0),     # 32 prompt pages, 6 attended per step
+    (2, 28, 4, 128, 256, 160, 448, 4, 8),    # Qwen group, 16 prompt pages
+    (1, 4, 2, 64, 160, 120, 256, 3, 0),      # d = 64, 10 prompt pages
+])
+def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp):
+    """quest_prefill_pages = K (PAPER.md :173/:183, :237): GPU vs oracle, bit-exact state and
+    out within 2e-2 -- out would differ grossly if a different prompt page were selected."""
+    st = _long_prompt_stream(500 + P + K, B, Hq, Hkv, d, P, T)
+    gaps = []
+
+    def on_step(i, layer, oracle, g_out, o_out):
+        qs = oracle.get_selection()["qscore"]
+        for u in range(qs.shape[0]):
+            v = np.sort(qs[u][np.isfinite(qs[u])])[::-1]
+            if len(v) > K:
+                gaps.append((v[K - 1] - v[K]) / max(abs(v[K - 1]), 1e-30))
+
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, split_pages=sp,
+                                 quest_prefill_pages=K, on_step=on_step)
+    assert gaps and min(gaps) > 1e-5, "selection boundary too close for an fp32-vs-fp64 check"
+    assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0

@@ -597,3 +597,69 @@ def test_top_r_brute_force(oracle_mod, page, L, P, g, r):
             mine = sorted((p, int(state["start"][u, p]), int(state["count"][u, p]),
                            int(state["ts"][u, p])) for p in range(L // page) if state["count"][u, p] > 0)
             assert mine == ref[u][i], (u, i)
+
+
+# ---------------------------------------------------------------- NEXT-4: Quest-on-prefill hybrid
+
+
+def _hybrid_stream(seed, B=2, Hkv=2, g=2, d=32, n_prompt_pages=8, T=90):
+    """Prompt pages whose 16 keys are identical (so Quest's bound equals the exact logit),
+    random decode keys, random values and queries."""
+    rng = np.random.default_rng(seed)
+    from paper_2502_11147_b200.synth import Stream, bf16_bits
+    P = PAGE * n_prompt_pages
+    phi = rng.standard_normal((B, Hkv, n_prompt_pages, d)) * 0.7
+    k_pre = np.repeat(phi, PAGE, axis=2).astype(np.float32)
+    v_pre = rng.standard_normal((B, Hkv, P, d)).astype(np.float32)
+    q = rng.standard_normal((T, B, Hkv * g, d)).astype(np.float32) * 1.5
+    k = rng.standard_normal((T, B, Hkv, d)).astype(np.float32) * 0.5
+    v = rng.standard_normal((T, B, Hkv, d)).astype(np.float32)
+    return Stream(bf16_bits(k_pre), bf16_bits(v_pre), bf16_bits(q), bf16_bits(k), bf16_bits(v))
+
+
+def test_hybrid_selects_top_k_prompt_pages_and_attends_exactly_those(oracle_mod):
+    """Quest on the prompt + RaaS on decode (PAPER.md :173/:183, :237; reading D24).  With
+    constant keys inside each prompt page the bound is the exact logit, so the selection is
+    the K pages with the largest max_h q_h.phi_p, and out is textbook attention over the
+    selected prompt pages plus the resident decode tokens."""
+    B, Hkv, g, d, npp, T, K = 2, 2, 2, 32, 8, 90, 3
+    st = _hybrid_stream(3, B, Hkv, g, d, npp, T)
+    P, L = PAGE * npp, PAGE * npp + 64
+    o = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hkv * g, n_kv_heads=Hkv, head_dim=d,
+                          batch=B, quest_prefill_pages=K)
+    o.prefill(st.k_pre, st.v_pre, P)
+    Kp, Vp = positions_kv(st)
+    scale = 1.0 / math.sqrt(d)
+    phi = bf16_to_f32(st.k_pre)[:, :, ::PAGE].astype(np.float64)     # [B, Hkv, npp, d]
+    for i in range(T):
+        out = o.decode_step(st.q[i], st.k[i], st.v[i])
+        sel = o.get_selection()
+        q = bf16_to_f32(st.q[i]).astype(np.float64)
+        for b in range(B):
+            for kv in range(Hkv):
+                u = b * Hkv + kv
+                sc = np.max(np.einsum("hd,pd->hp", q[b, kv * g:(kv + 1) * g], phi[b, kv]), axis=0)
+                top = sorted(np.argsort(-sc, kind="stable")[:K].tolist())
+                assert np.flatnonzero(sel["attended"][u, :npp]).tolist() == top
+                res = o.resident_positions(u)
+                att = [x for x in res if x > P or (x - 1) // PAGE in top]
+                idx = np.array(att) - 1
+                for j in range(g):
+                    ref = textbook_attention(q[b, kv * g + j], Kp[b, kv, idx], Vp[b, kv, idx], scale)
+                    assert np.abs(ref - out[b, kv * g + j]).max() < 1e-12
+
+
+def test_hybrid_with_k_at_least_prompt_pages_is_plain_raas(oracle_mod):
+    st = _hybrid_stream(4)
+    P, L = PAGE * 8, PAGE * 8 + 64
+    outs, states = [], []
+    for K in (0, 8, 20):
+        o = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=4, n_kv_heads=2, head_dim=32,
+                              batch=2, quest_prefill_pages=K)
+        o.prefill(st.k_pre, st.v_pre, P)
+        outs.append(np.stack([o.decode_step(st.q[i], st.k[i], st.v[i]) for i in range(st.T)]))
+        states.append(o.get_state())
+    for x in outs[1:]:
+        assert np.array_equal(x, outs[0])
+    for s_ in states[1:]:
+        assert all(np.array_equal(s_[k], states[0][k]) for k in s_)
