@@ -483,5 +483,7 @@ def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp
 
     res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-4, Hq=Hq, Hkv=Hkv, split_pages=sp,
                                  quest_prefill_pages=K, on_step=on_step)
-    assert gaps and min(gaps) > 1e-5, "selection boundary too close for an fp32-vs-fp64 check"
+    # fp32 bound sums carry ~1e-7 relative error: a closer K-th/(K+1)-th gap could flip the
+    # selection (the data are seeded, so this holds or fails deterministically)
+    assert gaps and min(gaps) > 2e-6, "selection boundary too close for an fp32-vs-fp64 check"
     assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
