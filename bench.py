@@ -227,7 +227,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     sp = args.split_pages if args.split_pages else cfg.get("split_pages", 0)
     score_mode = 1 if args.score == "quest" else 0
     layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode,
-                        stamp_rule=1 if args.top_r > 0 else 0, top_r=args.top_r)
+                        stamp_rule=1 if args.top_r > 0 else 0, top_r=args.top_r,
+                        quest_prefill_pages=args.quest_prefill)
               for _ in range(nl)]
     info = layers[0].raas_launch_info()
     for ly in layers:
@@ -321,7 +322,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         occ_mean = L - 7.5
     else:
         occ_mean = float(occ_now)
-    bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * C)
+    nfull = P // 16
+    if args.quest_prefill and nfull > args.quest_prefill:
+        # hybrid: only K of the nfull prompt pages are read, plus their representative keys
+        occ_mean -= (nfull - args.quest_prefill) * 16
+        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * C + nfull * 4 * d)
+    else:
+        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * C)
     launch_s = ms_per_step / 1e3 / nl
     achieved = bytes_launch / launch_s / 1e9
     peak, peak_src = measured_peaks()
@@ -396,6 +403,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
                    "page": 16, "alpha": args.alpha, "score_mode": args.score,
                    "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
+                   "quest_prefill_pages": args.quest_prefill,
                    "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
                                    if heads else f"request-sharded x{world}, no collective"),
                    "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
@@ -475,6 +483,9 @@ def main():
     ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
                     help="multi-GPU: shard requests (weak scaling) or kv-heads (strong, all-gather)")
     ap.add_argument("--split-pages", type=int, default=0, help="override pages per split tile")
+    ap.add_argument("--quest-prefill", type=int, default=0,
+                    help="Quest-on-prefill hybrid: prompt pages attended per step (NEXT-4)")
+    ap.add_argument("--P", type=int, default=0, help="override the prompt length")
     ap.add_argument("--top-r", type=float, default=0.0,
                     help="stamp the top r fraction of pages instead of the alpha threshold (NEXT-3)")
     ap.add_argument("--score", default="exact", choices=["exact", "quest"],
@@ -493,6 +504,9 @@ def main():
         args.fill = 0
     if args.batch:
         cfg["batch"] = args.batch
+    if args.P:
+        cfg["P"] = args.P
+        cfg["workload"] += f"_P{args.P}"
     if args.layers:
         cfg["layers"] = args.layers
     args.warmup = max(args.warmup, 3)

@@ -464,8 +464,8 @@ def _long_prompt_stream(seed, B, Hq, Hkv, d, P, T):
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,K,sp", [
-    (2, 8, 2, 128, 512, 200, 768, 6, 0),     # 32 prompt pages, 6 attended per step
-    (2, 28, 4, 128, 256, 160, 448, 4, 8),    # Qwen group, 16 prompt pages
+    (2, 8, 2, 128, 512, 200, 640, 6, 0),     # 32 prompt pages, 6 attended per step
+    (2, 28, 4, 128, 256, 160, 384, 4, 8),    # Qwen group, 16 prompt pages
     (1, 4, 2, 64, 160, 120, 256, 3, 0),      # d = 64, 10 prompt pages
 ])
 def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp):
