@@ -52,7 +52,7 @@ template <int D>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
-  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, qscore, vmap, counter, pmax, part_acc, part_ml, status, sched,
+  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, pmax, part_acc, part_ml, status, sched,
       stats, sq, sk, sv, so, total;
 };
 
@@ -113,7 +113,6 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.nfull = take(U * 4);
   const bool hyb = c->quest_prefill_pages > 0;  // Quest-on-prefill hybrid workspace (NEXT-4)
   L.repkey = hyb ? take(U * C * 2 * D * 2) : 0;
-  L.qscore = hyb ? take(U * C * 4) : 0;
   L.vmap = hyb ? take(U * C * 4) : 0;
   L.plen = take((size_t)c->batch * 4);
   L.plan = take(U * 16);
@@ -232,18 +231,20 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.log2_alpha = h->cfg.alpha > 0.f ? log2f(h->cfg.alpha) : -INFINITY;
 
   if (p.quest_k > 0) {  // hybrid: this step's prompt-page selection from q (D24)
-    const int units = h->d.units, C = h->d.C;
-    const int chunks = (C + 31) / 32;
-    const long long warps = (long long)units * chunks;
-    raas::raas_qbound_kernel<D><<<(int)((warps + 7) / 8), 256, 0, st>>>(
-        p.q, reinterpret_cast<const __nv_bfloat16*>(a + h->lay.repkey), p.nfull,
-        reinterpret_cast<float*>(a + h->lay.qscore), units, C, p.g, p.quest_k);
-    RAAS_CUDA(cudaGetLastError());
-    const int wpb = 4;
-    raas::raas_qselect_kernel<<<(units + wpb - 1) / wpb, 32 * wpb, wpb * (8 * C + 1024), st>>>(
-        reinterpret_cast<const float*>(a + h->lay.qscore), p.nfull,
-        reinterpret_cast<int32_t*>(a + h->lay.vmap), units, C, p.quest_k);
-    RAAS_CUDA(cudaGetLastError());
+    const int units = h->d.units, C = h->d.C, wpb = 4;
+    cudaLaunchConfig_t qc{};
+    qc.gridDim = dim3((units + wpb - 1) / wpb);
+    qc.blockDim = dim3(32 * wpb);
+    qc.dynamicSmemBytes = wpb * (8 * C + 1024);
+    qc.stream = st;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    qa[0].val.programmaticStreamSerializationAllowed = 1;
+    qc.attrs = qa;
+    qc.numAttrs = 1;
+    RAAS_CUDA(cudaLaunchKernelEx(&qc, raas::raas_qselect_kernel<D>, p.q,
+                                 reinterpret_cast<const __nv_bfloat16*>(a + h->lay.repkey), p.nfull,
+                                 reinterpret_cast<int32_t*>(a + h->lay.vmap), units, C, p.g, p.quest_k));
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(h->grid);

@@ -286,59 +286,19 @@ __global__ void raas_repkey_kernel(const __nv_bfloat16* __restrict__ kvstore,
   }
 }
 
-// Quest bound of every full prompt page: max over the group's heads of
-// sum_c max(q_c min_c, q_c max_c).  One warp per (unit, 32 pages), a lane per page.
+// Per step: Quest bound of every full prompt page (max over the group's heads of
+// sum_c max(q_c min_c, q_c max_c)) and the top-K pages by (bound desc, page asc) ->
+// vmap[u][0..K) in ascending page order.  One warp per unit, a lane per page; shared memory
+// per warp: 8*C bytes of ranking keys + 1 KiB histogram.  PDL-chained in front of the decode
+// kernel.
 template <int D>
-__global__ void raas_qbound_kernel(const __nv_bfloat16* __restrict__ q,
-                                   const __nv_bfloat16* __restrict__ repkey,
-                                   const int32_t* __restrict__ nfull, float* qscore, int units,
-                                   int C, int g, int K) {
-  const int wid = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  const int chunks = (C + 31) / 32;
-  const int u = wid / chunks, c0 = (wid - u * chunks) * 32;
-  if (u >= units) return;
-  const int nf = nfull[u];
-  if (nf <= K || c0 >= nf) return;
-  const int pg = c0 + lane;
-  const bool ok = pg < nf;
-  float U[MAX_GROUP];
-#pragma unroll
-  for (int h = 0; h < MAX_GROUP; ++h) U[h] = 0.f;
-  const size_t pu = (size_t)u * C + (ok ? pg : 0);
-  for (int c8 = 0; c8 < D / 8; ++c8) {
-    const uint4 mnv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 0) * D) + c8);
-    const uint4 mxv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 1) * D) + c8);
-    const uint32_t mnw[4] = {mnv.x, mnv.y, mnv.z, mnv.w}, mxw[4] = {mxv.x, mxv.y, mxv.z, mxv.w};
-#pragma unroll
-    for (int h = 0; h < MAX_GROUP; ++h) {
-      if (h < g) {
-        const uint4 qv = __ldg(reinterpret_cast<const uint4*>(q + ((size_t)u * g + h) * D) + c8);
-        const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t sh = (e & 1) ? 0u : 16u;
-          const float qf = __uint_as_float((qw[e >> 1] << sh) & 0xffff0000u);
-          const float a = __uint_as_float((mnw[e >> 1] << sh) & 0xffff0000u);
-          const float b = __uint_as_float((mxw[e >> 1] << sh) & 0xffff0000u);
-          U[h] += fmaxf(qf * a, qf * b);
-        }
-      }
-    }
-  }
-  float sc = -INFINITY;
-#pragma unroll
-  for (int h = 0; h < MAX_GROUP; ++h)
-    if (h < g) sc = fmaxf(sc, U[h]);
-  if (ok) qscore[(size_t)u * C + pg] = sc;
-}
-
-// Top-K full prompt pages by (bound desc, page asc) -> vmap[u][0..K) in ascending page order.
-// One warp per unit; shared memory: per warp 8*C bytes of keys + 1 KiB histogram.
-__global__ void raas_qselect_kernel(const float* __restrict__ qscore,
+__global__ void raas_qselect_kernel(const __nv_bfloat16* __restrict__ q,
+                                    const __nv_bfloat16* __restrict__ repkey,
                                     const int32_t* __restrict__ nfull, int32_t* vmap, int units,
-                                    int C, int K) {
+                                    int C, int g, int K) {
   extern __shared__ uint8_t qs_smem[];
+  pdl_wait();  // q of this step / repkeys are written by earlier work in the stream
+  pdl_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.x * (blockDim.x >> 5) + warp;
   if (u >= units) return;
@@ -347,7 +307,35 @@ __global__ void raas_qselect_kernel(const float* __restrict__ qscore,
   const uint32_t keys = smem_u32(qs_smem) + warp * (8 * C + 1024);
   const uint32_t hist = keys + 8 * C;
   for (int pg = lane; pg < nf; pg += 32) {
-    const unsigned long long key = rank_key(qscore[(size_t)u * C + pg], (uint32_t)pg);
+    const size_t pu = (size_t)u * C + pg;
+    float U[MAX_GROUP];
+#pragma unroll
+    for (int h = 0; h < MAX_GROUP; ++h) U[h] = 0.f;
+    for (int c8 = 0; c8 < D / 8; ++c8) {
+      const uint4 mnv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 0) * D) + c8);
+      const uint4 mxv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 1) * D) + c8);
+      const uint32_t mnw[4] = {mnv.x, mnv.y, mnv.z, mnv.w}, mxw[4] = {mxv.x, mxv.y, mxv.z, mxv.w};
+#pragma unroll
+      for (int h = 0; h < MAX_GROUP; ++h) {
+        if (h < g) {
+          const uint4 qv = __ldg(reinterpret_cast<const uint4*>(q + ((size_t)u * g + h) * D) + c8);
+          const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t sh = (e & 1) ? 0u : 16u;
+            const float qf = __uint_as_float((qw[e >> 1] << sh) & 0xffff0000u);
+            const float a = __uint_as_float((mnw[e >> 1] << sh) & 0xffff0000u);
+            const float b = __uint_as_float((mxw[e >> 1] << sh) & 0xffff0000u);
+            U[h] += fmaxf(qf * a, qf * b);
+          }
+        }
+      }
+    }
+    float sc = -INFINITY;
+#pragma unroll
+    for (int h = 0; h < MAX_GROUP; ++h)
+      if (h < g) sc = fmaxf(sc, U[h]);
+    const unsigned long long key = rank_key(sc, (uint32_t)pg);
     asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys + 8 * pg), "l"(key) : "memory");
   }
   __syncwarp();
