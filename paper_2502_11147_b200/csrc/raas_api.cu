@@ -231,11 +231,11 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.log2_alpha = h->cfg.alpha > 0.f ? log2f(h->cfg.alpha) : -INFINITY;
 
   if (p.quest_k > 0) {  // hybrid: this step's prompt-page selection from q (D24)
-    const int units = h->d.units, C = h->d.C, wpb = 4;
+    const int units = h->d.units, C = h->d.C;
     cudaLaunchConfig_t qc{};
-    qc.gridDim = dim3((units + wpb - 1) / wpb);
-    qc.blockDim = dim3(32 * wpb);
-    qc.dynamicSmemBytes = wpb * (8 * C + 1024);
+    qc.gridDim = dim3(units);
+    qc.blockDim = dim3(128);
+    qc.dynamicSmemBytes = p.g * D * 4 + 8 * C + 1024;
     qc.stream = st;
     cudaLaunchAttribute qa[1];
     qa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -288,57 +288,77 @@ __global__ void raas_repkey_kernel(const __nv_bfloat16* __restrict__ kvstore,
 
 // Per step: Quest bound of every full prompt page (max over the group's heads of
 // sum_c max(q_c min_c, q_c max_c)) and the top-K pages by (bound desc, page asc) ->
-// vmap[u][0..K) in ascending page order.  One warp per unit, a lane per page; shared memory
-// per warp: 8*C bytes of ranking keys + 1 KiB histogram.  PDL-chained in front of the decode
+// vmap[u][0..K) in ascending page order.  One 128-thread block per unit: 8 lanes per page for
+// the bounds (q staged in shared memory as fp32), then warp 0 selects.  Shared memory:
+// g*D*4 (q) + 8*C (ranking keys) + 1 KiB (histogram).  PDL-chained in front of the decode
 // kernel.
 template <int D>
-__global__ void raas_qselect_kernel(const __nv_bfloat16* __restrict__ q,
+__global__ void __launch_bounds__(128) raas_qselect_kernel(const __nv_bfloat16* __restrict__ q,
                                     const __nv_bfloat16* __restrict__ repkey,
                                     const int32_t* __restrict__ nfull, int32_t* vmap, int units,
                                     int C, int g, int K) {
   extern __shared__ uint8_t qs_smem[];
-  pdl_wait();  // q of this step / repkeys are written by earlier work in the stream
+  pdl_wait();  // q of this step is produced by earlier work in the stream
   pdl_launch_dependents();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (u >= units) return;
+  const int u = blockIdx.x;
   const int nf = nfull[u];
-  if (nf <= K) return;
-  const uint32_t keys = smem_u32(qs_smem) + warp * (8 * C + 1024);
+  if (nf <= K) return;  // block-uniform
+  float* qf = reinterpret_cast<float*>(qs_smem);
+  const uint32_t keys = smem_u32(qs_smem) + g * D * 4;
   const uint32_t hist = keys + 8 * C;
-  for (int pg = lane; pg < nf; pg += 32) {
-    const size_t pu = (size_t)u * C + pg;
-    float U[MAX_GROUP];
+  for (int i = threadIdx.x; i < g * D; i += blockDim.x)
+    qf[i] = __bfloat162float(q[(size_t)u * g * D + i]);
+  __syncthreads();
+  // 8 lanes per page, each over D/8 channels; 16 pages per pass of the 128-thread block
+  constexpr int CH = D / 8;  // channels per lane
+  const int sub = threadIdx.x >> 3, cl = threadIdx.x & 7;
+  for (int p0 = 0; p0 < nf; p0 += 16) {
+    const int pg = p0 + sub;
+    const bool ok = pg < nf;
+    const size_t pu = (size_t)u * C + (ok ? pg : 0);
+    const __nv_bfloat16* mnp = repkey + (pu * 2 + 0) * D + cl * CH;
+    const __nv_bfloat16* mxp = repkey + (pu * 2 + 1) * D + cl * CH;
+    uint32_t mnw[CH / 2], mxw[CH / 2];
 #pragma unroll
-    for (int h = 0; h < MAX_GROUP; ++h) U[h] = 0.f;
-    for (int c8 = 0; c8 < D / 8; ++c8) {
-      const uint4 mnv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 0) * D) + c8);
-      const uint4 mxv = __ldg(reinterpret_cast<const uint4*>(repkey + (pu * 2 + 1) * D) + c8);
-      const uint32_t mnw[4] = {mnv.x, mnv.y, mnv.z, mnv.w}, mxw[4] = {mxv.x, mxv.y, mxv.z, mxv.w};
-#pragma unroll
-      for (int h = 0; h < MAX_GROUP; ++h) {
-        if (h < g) {
-          const uint4 qv = __ldg(reinterpret_cast<const uint4*>(q + ((size_t)u * g + h) * D) + c8);
-          const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t sh = (e & 1) ? 0u : 16u;
-            const float qf = __uint_as_float((qw[e >> 1] << sh) & 0xffff0000u);
-            const float a = __uint_as_float((mnw[e >> 1] << sh) & 0xffff0000u);
-            const float b = __uint_as_float((mxw[e >> 1] << sh) & 0xffff0000u);
-            U[h] += fmaxf(qf * a, qf * b);
-          }
-        }
-      }
+    for (int v = 0; v < CH / 8; ++v) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(mnp) + v);
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(mxp) + v);
+      mnw[4 * v] = a.x; mnw[4 * v + 1] = a.y; mnw[4 * v + 2] = a.z; mnw[4 * v + 3] = a.w;
+      mxw[4 * v] = b.x; mxw[4 * v + 1] = b.y; mxw[4 * v + 2] = b.z; mxw[4 * v + 3] = b.w;
     }
     float sc = -INFINITY;
 #pragma unroll
-    for (int h = 0; h < MAX_GROUP; ++h)
-      if (h < g) sc = fmaxf(sc, U[h]);
-    const unsigned long long key = rank_key(sc, (uint32_t)pg);
-    asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys + 8 * pg), "l"(key) : "memory");
+    for (int h = 0; h < MAX_GROUP; ++h) {
+      if (h < g) {
+        const float4* qh = reinterpret_cast<const float4*>(qf + h * D + cl * CH);
+        float U = 0.f;
+#pragma unroll
+        for (int c4 = 0; c4 < CH / 4; ++c4) {
+          const float4 qv = qh[c4];
+          const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = 4 * c4 + e;
+            const uint32_t sh = (c & 1) ? 0u : 16u;
+            const float a = __uint_as_float((mnw[c >> 1] << sh) & 0xffff0000u);
+            const float b = __uint_as_float((mxw[c >> 1] << sh) & 0xffff0000u);
+            U += fmaxf(qa[e] * a, qa[e] * b);
+          }
+        }
+        U += __shfl_xor_sync(0xffffffffu, U, 1);
+        U += __shfl_xor_sync(0xffffffffu, U, 2);
+        U += __shfl_xor_sync(0xffffffffu, U, 4);
+        sc = fmaxf(sc, U);
+      }
+    }
+    if (ok && cl == 0) {
+      const unsigned long long key = rank_key(sc, (uint32_t)pg);
+      asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys + 8 * pg), "l"(key) : "memory");
+    }
   }
-  __syncwarp();
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   const unsigned long long kth = warp_kth_largest(keys, hist, nf, K, lane);
   int base = 0;
   for (int c0 = 0; c0 < nf; c0 += 32) {  // ascending compaction of the selected pages
