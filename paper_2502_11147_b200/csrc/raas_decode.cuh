@@ -420,6 +420,20 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     fence_mbar_init();
   }
   __syncthreads();
+  if (warp == 0 && p.quest_k == 0) {
+    // Warm L2 with this CTA's first owned tile while the previous kernel drains (its tail
+    // leaves HBM idle).  Only a hint: nothing is read from these lines before griddepcontrol.wait
+    // below, and L2 is the point of coherence, so a row the previous kernel rewrites is seen.
+    const int fu = p.units / (int)gridDim.x;
+    if (fu > 0) {
+      const int unit0 = blockIdx.x * fu;
+      for (int pg = lane; pg < min(p.split_pages, p.C); pg += 32)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         p.kvstore + ((size_t)unit0 * p.C + pg) * 2 * PAGE * D),
+                     "r"(2 * PAGE * D * 2)
+                     : "memory");
+    }
+  }
   pdl_wait();  // everything above overlapped the previous kernel; state reads start here
   pdl_launch_dependents();
   const long long t_start = dbg_clock();
