@@ -25,6 +25,10 @@
 //                  the <= 8 q-heads of the GQA group = N), online softmax in fp32 registers.
 #pragma once
 
+#ifndef RAAS_PREFETCH_TILES
+#define RAAS_PREFETCH_TILES 2  // owned tiles warmed in L2 before griddepcontrol.wait
+#endif
+
 namespace raas {
 
 #ifdef RAAS_DBG_TIMING  // tuning experiment: per-CTA cycle accounting of the pipeline waits
@@ -427,9 +431,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     const int fu = p.units / (int)gridDim.x;
     if (fu > 0) {
       const int unit0 = blockIdx.x * fu;
-      for (int pg = lane; pg < min(p.split_pages, p.C); pg += 32)
+      for (int pg = lane; pg < min(RAAS_PREFETCH_TILES * p.split_pages, fu * p.C); pg += 32)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                         p.kvstore + ((size_t)unit0 * p.C + pg) * 2 * PAGE * D),
+                         p.kvstore + ((size_t)unit0 * p.C + pg) * 2 * PAGE * D),  // unit-major
                      "r"(2 * PAGE * D * 2)
                      : "memory");
     }
