@@ -425,7 +425,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "timing": "CUDA events on the launch stream around K graph replays of "
                                f"{nl} launches; avg launch = step / {nl}"},
         "e2e": e2e,
-        "gpu_launches": args.steps * nl,
+        "gpu_launches": args.steps * nl * (2 if args.quest_prefill else 1),
         "launch": info,
         "stamp_rate": stamps / max(decisions, 1),
         "evictions_per_step": evictions / max(unit_steps, 1) * units,

@@ -6,7 +6,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baselin
 
 This module is a thin ctypes loader for ``raas_ref.c`` (plain C, fp64), which follows
 PAPER.md §3.3 / App. B step by step (see the C file for citations and DESIGN.md §3 for
-the readings D1-D20).
+the readings D1-D24).
 """
 from __future__ import annotations
 

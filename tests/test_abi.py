@@ -68,6 +68,24 @@ def test_arena_bytes(L, cfg, expect):
         assert kv <= n <= kv * 1.2 + (1 << 20)   # O(L): the KV store dominates
 
 
+@pytest.mark.parametrize("extra", [dict(score_mode=2), dict(stamp_rule=3), dict(stamp_rule=1, top_r=1.5),
+                                   dict(quest_prefill_pages=-1), dict(split_pages=33),
+                                   dict(stamp_rule=1, top_r=0.5, L=16384),
+                                   dict(quest_prefill_pages=8, L=16384)])
+def test_arena_bytes_rejects_bad_modes(L, extra):
+    base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
+    base.update(extra)
+    assert raas.raas_arena_bytes(raas.make_config(**base)) == 0
+
+
+def test_hybrid_mode_adds_representative_keys_only(L):
+    base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
+    a0 = raas.raas_arena_bytes(raas.make_config(**base))
+    a1 = raas.raas_arena_bytes(raas.make_config(**base, quest_prefill_pages=16))
+    kv = 2 * 16 * 128 * 2 * 2 * 128 * 16   # units x pages x (K+V rows) bytes
+    assert 0 < a1 - a0 <= kv / 16 + 2 * 16 * 128 * 4 + 4096   # min/max keys (1/16 of K) + vmap
+
+
 def test_arena_is_linear_in_L_not_N(L):
     """Memory plateaus at the budget (PAPER.md :191-193): the arena depends on L only."""
     a = [raas.raas_arena_bytes(raas.make_config(L=L_, alpha=1e-4, n_q_heads=32, n_kv_heads=8,
