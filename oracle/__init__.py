@@ -51,6 +51,7 @@ class _Cfg(ctypes.Structure):
         ("stamp_rule", ctypes.c_int32),
         ("top_r", ctypes.c_double),
         ("quest_prefill_pages", ctypes.c_int32),
+        ("table_scope", ctypes.c_int32),
     ]
 
 
@@ -98,9 +99,9 @@ class Oracle:
 
     def __init__(self, L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch,
                  softmax_scale=0.0, score_mode=0, stamp_rule=0, top_r=0.5,
-                 quest_prefill_pages=0):
+                 quest_prefill_pages=0, table_scope=0):
         self.cfg = _Cfg(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
-                        score_mode, stamp_rule, top_r, quest_prefill_pages)
+                        score_mode, stamp_rule, top_r, quest_prefill_pages, table_scope)
         self.C = L // page if page > 0 else 0
         self.units = batch * n_kv_heads
         self.page, self.d, self.hq, self.hkv, self.batch = page, head_dim, n_q_heads, n_kv_heads, batch

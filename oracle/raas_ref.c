@@ -3,7 +3,7 @@
  * (see raas_ref.h).  Plain, slow, fp64, one unit at a time; no blocking, no fusion,
  * no streaming softmax.  Each block cites the passage it follows.
  *
- * Algorithm (readings D1-D20 in DESIGN.md §3):
+ * Algorithm (readings D1-D25 in DESIGN.md §3):
  *   prefill(P):  pages 0..Pp-1 hold positions 1..P in order, 16 per page; they are
  *                pinned ("Pages corresponding to prefill tokens are exempt from
  *                eviction", App. B :396); t = P (time = number of tokens,
@@ -39,6 +39,7 @@ typedef struct {
   int32_t nfull;          /* full prompt pages (selectable in the hybrid mode) */
   uint8_t *attended;      /* [C] hybrid trace */
   double *qscore;         /* [C] hybrid trace */
+  double *best;           /* [C] decisive log-score of the last step (before the stamp) */
 } ref_unit;
 
 struct raas_ref {
@@ -81,6 +82,7 @@ int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
   if (cfg->stamp_rule != 0 && cfg->stamp_rule != 1) return REF_E_INVALID;
   if (cfg->stamp_rule == 1 && !(cfg->top_r >= 0.0 && cfg->top_r <= 1.0)) return REF_E_INVALID;
   if (cfg->quest_prefill_pages < 0) return REF_E_INVALID;
+  if (cfg->table_scope != 0 && cfg->table_scope != 1) return REF_E_INVALID;
   raas_ref* h = (raas_ref*)calloc(1, sizeof *h);
   if (!h) return REF_E_INVALID;
   h->cfg = *cfg;
@@ -99,6 +101,7 @@ int raas_ref_create(const raas_ref_config* cfg, raas_ref** out) {
     u->pstar = (double*)calloc((size_t)h->C, sizeof(double));
     u->attended = (uint8_t*)calloc((size_t)h->C, 1);
     u->qscore = (double*)calloc((size_t)h->C, sizeof(double));
+    u->best = (double*)calloc((size_t)h->C, sizeof(double));
     u->K = (double*)calloc(kv, sizeof(double));
     u->V = (double*)calloc(kv, sizeof(double));
     u->cur = -1;
@@ -115,6 +118,7 @@ void raas_ref_destroy(raas_ref* h) {
     ref_unit* u = &h->u[i];
     free(u->start); free(u->count); free(u->ts); free(u->pinned);
     free(u->pstar); free(u->K); free(u->V); free(u->attended); free(u->qscore);
+    free(u->best);
   }
   free(h->u);
   free(h);
@@ -221,7 +225,7 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
   select_and_write(h, u, k_new + (size_t)ui * d, v_new + (size_t)ui * d);
 
   double* s = (double*)malloc((size_t)C * page * sizeof(double));
-  double* best = (double*)malloc((size_t)C * sizeof(double));
+  double* best = u->best;
   double* qh = (double*)malloc((size_t)d * sizeof(double));
   for (int32_t p = 0; p < C; ++p) best[p] = -INFINITY;
 
@@ -320,6 +324,13 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
       if (lp > best[p]) best[p] = lp;
     }
   }
+  free(s); free(qh);
+}
+
+/* a6 for one unit, given the decisive log-score best[p] of every page: the unit's own
+ * (table_scope 0) or the maximum over the request's kv-heads (table_scope 1, D25). */
+static void stamp_unit(raas_ref* h, ref_unit* u, const double* best) {
+  const int32_t C = h->C;
   /* stamp: "we assign it the latest timestamp" when the score is above alpha (:29, :98,
    * :364), strictly (D3), in the log domain s - LSE > ln(alpha) (D2). */
   const double ln_alpha = log(h->cfg.alpha);     /* alpha = 0 -> -inf: every page stamped */
@@ -357,7 +368,6 @@ static void decode_unit(raas_ref* h, int32_t ui, const uint16_t* q, const uint16
     }
     free(taken);
   }
-  free(s); free(best); free(qh);
 }
 
 int raas_ref_decode_step(raas_ref* h, const uint16_t* q, const uint16_t* k_new,
@@ -367,6 +377,24 @@ int raas_ref_decode_step(raas_ref* h, const uint16_t* q, const uint16_t* k_new,
   int32_t ui;
 #pragma omp parallel for schedule(static) num_threads(g_threads)
   for (ui = 0; ui < h->units; ++ui) decode_unit(h, ui, q, k_new, v_new, out);
+  if (h->cfg.table_scope == 0) {
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+    for (ui = 0; ui < h->units; ++ui) stamp_unit(h, &h->u[ui], h->u[ui].best);
+  } else {
+    /* one page table per request: "tokens" of the layer are stamped when any head's score
+     * exceeds alpha (reading D25 of :29, :98 at request granularity) */
+    const int32_t Hkv = h->cfg.n_kv_heads, C = h->C;
+    double* rb = (double*)malloc((size_t)C * sizeof(double));
+    for (int32_t b = 0; b < h->cfg.batch; ++b) {
+      for (int32_t p = 0; p < C; ++p) {
+        rb[p] = -INFINITY;
+        for (int32_t kv = 0; kv < Hkv; ++kv)
+          if (h->u[b * Hkv + kv].best[p] > rb[p]) rb[p] = h->u[b * Hkv + kv].best[p];
+      }
+      for (int32_t kv = 0; kv < Hkv; ++kv) stamp_unit(h, &h->u[b * Hkv + kv], rb);
+    }
+    free(rb);
+  }
   return REF_OK;
 }
 

@@ -7,7 +7,7 @@
  *
  * What it computes: page-based RaaS (§3.3 :143-151, App. B :358-398) one
  * decode step at a time, in fp64, following SURVEY.md §8(c1) step by step, with the
- * readings D1-D20 listed in DESIGN.md §3.  Every tensor is a HOST buffer; bf16 values
+ * readings D1-D25 listed in DESIGN.md §3.  Every tensor is a HOST buffer; bf16 values
  * are passed as their raw uint16 bit patterns and widened exactly to double.
  *
  * Layouts (row-major):
@@ -52,6 +52,13 @@ typedef struct {
                             only the K full prompt pages with the largest representative-key
                             bound max_h sum_c max(q_hc min_c, q_hc max_c) (ties: lower page), plus
                             every other resident page; the prompt's KV stays resident */
+  int32_t table_scope;   /* granularity of the page table (reading D5 / D25):
+                            0 = one table per (request, kv-head), stamp if any q-head of the
+                                GQA group exceeds the threshold (default);
+                            1 = one table per request (per layer), shared by all its kv-heads:
+                                a page is stamped if ANY of the request's q-heads exceeds it,
+                                every kv-head evicts the same page.  The per-unit
+                                state arrays then hold identical replicas. */
 } raas_ref_config;
 
 typedef struct raas_ref raas_ref;

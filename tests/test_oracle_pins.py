@@ -309,16 +309,20 @@ def test_p5_bookkeeping_enumeration(oracle_mod, page, P, L, T):
 # ---------------------------------------------------------------- P6 brute-force end-to-end
 
 
-def brute_force_end_to_end(stream, L, alpha, page, g):
+def brute_force_end_to_end(stream, L, alpha, page, g, scope=0):
     """From-scratch simulator: token positions, direct exp/sum per step (no streaming
-    LSE), stamp iff exp(s - LSE) > alpha, evict min (ts, first position)."""
+    LSE), stamp iff exp(s - LSE) > alpha, evict min (ts, first position).
+    scope 0: one page table per (request, kv-head); scope 1: one table per request shared by
+    all its kv-heads, stamped if any of its q-heads exceeds alpha (D25).  Returns, per unit
+    (request, kv-head), the per-step (state snapshot, evicted position, outputs, margin)."""
     K, V = positions_kv(stream)
     B, Hkv, P, d = stream.k_pre.shape
     C, Pp = L // page, -(-P // page)
     scale = 1.0 / math.sqrt(d)
-    res = []
+    tables = [[kv] for kv in range(Hkv)] if scope == 0 else [list(range(Hkv))]
+    res = {}
     for b in range(B):
-        for kv in range(Hkv):
+        for kvs in tables:
             pages = []  # dicts: positions, ts, pinned, slot
             for p in range(Pp):
                 pages.append(dict(pos=list(range(p * page + 1, min(p * page + page, P) + 1)),
@@ -346,21 +350,24 @@ def brute_force_end_to_end(stream, L, alpha, page, g):
                 q = bf16_to_f32(stream.q[i, b]).astype(np.float64)
                 allpos = sorted(x for pg in pages for x in pg["pos"])
                 idx = np.array(allpos) - 1
-                outs, probs = [], []
-                for j in range(g):
-                    s = scale * (K[b, kv, idx] @ q[kv * g + j])
-                    e = np.exp(s)
-                    pr = e / e.sum()
-                    outs.append(pr @ V[b, kv, idx])
-                    probs.append(dict(zip(allpos, pr)))
+                outs, probs = {}, []
+                for kv in kvs:
+                    outs[kv] = []
+                    for j in range(g):
+                        s = scale * (K[b, kv, idx] @ q[kv * g + j])
+                        e = np.exp(s)
+                        pr = e / e.sum()
+                        outs[kv].append(pr @ V[b, kv, idx])
+                        probs.append(dict(zip(allpos, pr)))
                 for pg in pages:
                     if not pg["pinned"] and any(pr[x] > alpha for pr in probs for x in pg["pos"]):
                         pg["ts"] = t
                 margin = min(abs(pr[x] - alpha) for pr in probs for x in allpos)
                 snap = sorted((pg["slot"], pg["pos"][0], len(pg["pos"]), pg["ts"]) for pg in pages)
-                per_step.append((snap, ev, np.array(outs), margin))
-            res.append(per_step)
-    return res
+                per_step.append((snap, ev, {kv: np.array(o) for kv, o in outs.items()}, margin))
+            for kv in kvs:
+                res[b * Hkv + kv] = [(sn, ev, o[kv], m) for sn, ev, o, m in per_step]
+    return [res[u] for u in range(B * Hkv)]
 
 
 @pytest.mark.parametrize("page,L,P,g,alpha", [(1, 6, 2, 1, 0.12), (2, 6, 2, 2, 0.08), (1, 5, 1, 3, 0.15),
@@ -389,6 +396,56 @@ def test_p6_brute_force_end_to_end(oracle_mod, page, L, P, g, alpha):
             assert np.abs(out[b, kv * g:(kv + 1) * g] - outs).max() < 1e-12
             n_mixed += ev >= 0
     assert n_mixed > 0
+
+
+@pytest.mark.parametrize("page,L,P,Hkv,g,alpha", [(1, 6, 2, 2, 1, 0.12), (2, 6, 2, 3, 2, 0.08),
+                                                  (2, 8, 3, 2, 1, 0.1), (1, 5, 1, 4, 1, 0.15)])
+def test_request_table_brute_force(oracle_mod, page, L, P, Hkv, g, alpha):
+    """table_scope = 1 (D25): one page table per request, stamped by any of its
+    q-heads, pinned against the from-scratch simulator; every kv-head holds the same state."""
+    B, d, T = 2, 4, 8
+    st = gaussian_stream(300 + page * 10 + L + Hkv, B, g * Hkv, Hkv, d, P, T, sigma_q=2.0)
+    ref = brute_force_end_to_end(st, L, alpha, page, g, scope=1)
+    o = oracle_mod.Oracle(L=L, alpha=alpha, page=page, n_q_heads=g * Hkv, n_kv_heads=Hkv,
+                          head_dim=d, batch=B, table_scope=1)
+    o.prefill(st.k_pre, st.v_pre, P)
+    n_mixed = 0
+    for i in range(T):
+        out = o.decode_step(st.q[i], st.k[i], st.v[i])
+        state, evs = o.get_state(), o.get_trace()["evicted"]
+        for u in range(B * Hkv):
+            b, kv = divmod(u, Hkv)
+            snap, ev, outs, margin = ref[u][i]
+            assert margin > 1e-9, "borderline draw; change the seed"
+            mine = sorted((p, int(state["start"][u, p]), int(state["count"][u, p]),
+                           int(state["ts"][u, p])) for p in range(L // page) if state["count"][u, p] > 0)
+            assert mine == snap, (u, i)
+            assert evs[u] == ev
+            assert np.abs(out[b, kv * g:(kv + 1) * g] - outs).max() < 1e-12
+            n_mixed += ev >= 0
+        for k in ("ts", "start", "count", "pinned"):   # replicas identical within a request
+            a = state[k].reshape(B, Hkv, -1)
+            assert (a == a[:, :1]).all()
+    assert n_mixed > 0
+
+
+def test_request_table_differs_from_per_head_tables(oracle_mod):
+    """The two granularities are different methods: on a stream whose kv-heads attend
+    different pages, per-head tables and the per-request table evict differently."""
+    B, Hkv, g, d, P, T, L = 1, 2, 1, 8, 16, 120, 64
+    st = gaussian_stream(7, B, g * Hkv, Hkv, d, P, T, sigma_q=3.0)
+    ev = []
+    for scope in (0, 1):
+        o = oracle_mod.Oracle(L=L, alpha=0.02, page=PAGE, n_q_heads=g * Hkv, n_kv_heads=Hkv,
+                              head_dim=d, batch=B, table_scope=scope)
+        o.prefill(st.k_pre, st.v_pre, P)
+        e = []
+        for i in range(T):
+            o.decode_step(st.q[i], st.k[i], st.v[i], want_out=False)
+            e.append(o.get_trace()["evicted"].copy())
+        ev.append(np.array(e))
+    assert (ev[1][:, 0] == ev[1][:, 1]).all()
+    assert not (ev[0][:, 0] == ev[0][:, 1]).all()
 
 
 # ---------------------------------------------------------------- errors
