@@ -213,6 +213,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     B, hq, hkv, d, L, P, nl = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["d"], cfg["L"], cfg["P"], cfg["layers"]
     g = hq // hkv
     heads = args.shard == "heads" and world > 1
+    if heads and args.table_scope:
+        raise SystemExit("--table-scope 1 shares one page table over a request's kv-heads; "
+                         "shard by requests")
     hq_full = hq
     if heads:  # this rank's kv-heads and their q-heads; out is all-gathered every layer-step
         from paper_2502_11147_b200.shard import gather_heads, head_range
@@ -228,7 +231,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     score_mode = 1 if args.score == "quest" else 0
     layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode,
                         stamp_rule=1 if args.top_r > 0 else 0, top_r=args.top_r,
-                        quest_prefill_pages=args.quest_prefill)
+                        quest_prefill_pages=args.quest_prefill, table_scope=args.table_scope)
               for _ in range(nl)]
     info = layers[0].raas_launch_info()
     for ly in layers:
@@ -404,6 +407,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "page": 16, "alpha": args.alpha, "score_mode": args.score,
                    "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
                    "quest_prefill_pages": args.quest_prefill,
+                   "table_scope": "request" if args.table_scope else "kv-head",
                    "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
                                    if heads else f"request-sharded x{world}, no collective"),
                    "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
@@ -490,6 +494,8 @@ def main():
                     help="stamp the top r fraction of pages instead of the alpha threshold (NEXT-3)")
     ap.add_argument("--score", default="exact", choices=["exact", "quest"],
                     help="page score for stamping: exact page max (D4) or Quest bound (NEXT-1)")
+    ap.add_argument("--table-scope", type=int, default=0, choices=[0, 1],
+                    help="1: one page table per request, OR over all heads (reading D25)")
     ap.add_argument("--dense", type=int, default=0,
                     help="dense comparator: prefill N tokens, L > N + steps (no eviction)")
     args = ap.parse_args()

@@ -91,10 +91,19 @@ typedef struct {
                             pages with the largest representative-key bound
                             max_h sum_c max(q_c min_c, q_c max_c) (ties: lower page), plus all
                             other resident pages; stamping / eviction are unchanged (prompt pages
-                            stay pinned and resident).  Adds two small launches per step
-                            (bound, selection) and 1/16 of the prompt's K bytes.  L <= 8192.
+                            stay pinned and resident).  Adds one small launch per step
+                            (bound + selection) and 1/16 of the prompt's K bytes.  L <= 8192.
                             With raas_set_state, every pinned page is treated as a full prompt
                             page. */
+  int32_t table_scope;   /* page-table granularity (reading D25):
+                            0 = one table per (request, kv-head), stamped when any q-head of the
+                                GQA group exceeds the threshold (reading D5, default);
+                            1 = one table per request (per layer handle), shared by all its
+                                kv-heads: a page is stamped when ANY q-head of the request
+                                exceeds it and every kv-head evicts the same page.  The state
+                                arrays keep one identical replica per kv-head; raas_set_state
+                                rejects replicas that differ.  Sharding a request's kv-heads over
+                                handles would need an exchange, so shard by request only. */
 } raas_config;
 
 /* Bytes of device memory the handle needs (KV store: per unit L/16 pages, each 16 K rows + 16 V

@@ -52,7 +52,7 @@ template <int D>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
 
 struct Layout {
-  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, pmax, part_acc, part_ml, status, sched,
+  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, req_x, req_ctr, pmax, part_acc, part_ml, status, sched,
       stats, sq, sk, sv, so, total;
 };
 
@@ -82,6 +82,7 @@ int derive(const raas_config* c, Derived* d) {
   if (c->stamp_rule == 1 && d->C > 512)
     return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports L <= 8192 (512 pages)");
   if (c->quest_prefill_pages < 0) return fail(RAAS_E_INVALID, "quest_prefill_pages must be >= 0");
+  if (c->table_scope != 0 && c->table_scope != 1) return fail(RAAS_E_INVALID, "table_scope must be 0 or 1");
   if (c->quest_prefill_pages > 0 && d->C > 512)
     return fail(RAAS_E_UNSUPPORTED, "the Quest-on-prefill hybrid supports L <= 8192 (512 pages)");
   d->units = c->batch * c->n_kv_heads;
@@ -117,6 +118,8 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.plen = take((size_t)c->batch * 4);
   L.plan = take(U * 16);
   L.counter = take(U * 4);
+  L.req_x = c->table_scope ? take((size_t)c->batch * C * 4) : 0;   // zeroed by raas_create
+  L.req_ctr = c->table_scope ? take((size_t)c->batch * 4) : 0;
   L.pmax = take(U * C * g * 4);
   L.part_acc = take(U * d.nsplit * g * D * 4);
   L.part_ml = take(U * d.nsplit * g * 8);
@@ -225,6 +228,10 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.quest_k = h->cfg.quest_prefill_pages;
   p.nfull = reinterpret_cast<const int32_t*>(a + h->lay.nfull);
   p.vmap = h->cfg.quest_prefill_pages > 0 ? reinterpret_cast<const int32_t*>(a + h->lay.vmap) : nullptr;
+  p.table_scope = h->cfg.table_scope;
+  p.n_kv = h->cfg.n_kv_heads;
+  p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;
+  p.req_ctr = h->cfg.table_scope ? reinterpret_cast<int32_t*>(a + h->lay.req_ctr) : nullptr;
   const float scale = h->cfg.softmax_scale > 0.f ? h->cfg.softmax_scale
                                                  : 1.0f / sqrtf((float)h->cfg.head_dim);
   p.scale_log2 = scale * 1.4426950408889634f;
@@ -524,6 +531,18 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
     }
     npin[u] = np;
     plan[u] = make_int4(0, 0, 0, t[u] + 1);
+  }
+  if (h->cfg.table_scope) {  // one table per request: the kv-heads' replicas must agree
+    const size_t Hkv = h->cfg.n_kv_heads;
+    for (size_t u = 0; u < U; ++u) {
+      const size_t r = u - u % Hkv;
+      if (u == r) continue;
+      if (t[u] != t[r] || std::memcmp(ts + u * C, ts + r * C, C * 4) ||
+          std::memcmp(start_pos + u * C, start_pos + r * C, C * 4) ||
+          std::memcmp(count + u * C, count + r * C, C * 4) || std::memcmp(pinned + u * C, pinned + r * C, C))
+        return fail(RAAS_E_INVALID, "table_scope 1: kv-head %zu of request %zu differs from kv-head 0",
+                    u % Hkv, u / Hkv);
+    }
   }
   uint8_t* a = h->arena;
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.ts, ts, U * C * 4, cudaMemcpyHostToDevice, st));

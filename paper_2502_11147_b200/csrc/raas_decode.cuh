@@ -120,6 +120,14 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+// order-preserving float <-> uint32 (0 is below every float: the identity of atomicMax)
+__device__ __forceinline__ uint32_t order_f32(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unorder_f32(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -195,6 +203,11 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   constexpr int PPL = 4;  // pages per lane per chunk
   int tsv[PPL], stv[PPL];
   float pmv[PPL][MAX_GROUP];
+  // table_scope 1 (D25): once every kv-head of the request has combined, the last one decides
+  // for all of them from the request-wide page scores req_x (then pmv[i][0], with LSE 0)
+  const int req = unit / p.n_kv;
+  uint32_t* const rx = p.req_x + (size_t)req * C;
+  bool rq = false;
   auto load_meta = [&](int pc, int lim) {
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
@@ -203,9 +216,15 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       const size_t ix = (size_t)unit * C + pg;
       tsv[i] = ok ? __ldcg(p.ts + ix) : 0;
       stv[i] = ok ? __ldcg(p.start + ix) : 0;
+      if (rq) {
+        pmv[i][0] = (ok && pg >= npin) ? unorder_f32(__ldcg(rx + pg)) : -INFINITY;
 #pragma unroll
-      for (int h = 0; h < MAX_GROUP; ++h)
-        pmv[i][h] = (ok && h < g) ? __ldcg(p.pmax + ix * g + h) : -INFINITY;
+        for (int h = 1; h < MAX_GROUP; ++h) pmv[i][h] = -INFINITY;
+      } else {
+#pragma unroll
+        for (int h = 0; h < MAX_GROUP; ++h)
+          pmv[i][h] = (ok && h < g) ? __ldcg(p.pmax + ix * g + h) : -INFINITY;
+      }
     }
   };
   load_meta(0, C);
@@ -255,6 +274,49 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     sts_f32(scr_inv + 4 * lane, 1.f / L);
   }
   __syncwarp();
+  float lse[MAX_GROUP];
+#pragma unroll
+  for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
+  // page score x_p = max_h (score_hp - LSE_h) (log2 domain).  Rule 0: stamp iff x_p > log2 a
+  // (strict, D3).  Rule 1 (top-r, PAPER.md :135, reading D23): stamp the k = ceil(r n) pages with
+  // the largest (x_p, -start_pos) among the n unpinned resident pages.
+  auto page_x = [&](int i) {
+    float x = -INFINITY;
+#pragma unroll
+    for (int h = 0; h < MAX_GROUP; ++h)
+      if (h < g) x = fmaxf(x, pmv[i][h] - lse[h]);
+    return x;
+  };
+  if (p.table_scope != 0) {
+    // table_scope 1 (D25): fold this kv-head's page scores into the request-wide maximum
+    // early, so the reductions drain while the output is combined
+    for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
+      if (pc > 0) load_meta(pc, used_eff);
+#pragma unroll
+      for (int i = 0; i < PPL; ++i) {
+        const int pg = pc + 32 * i + lane;
+        if (pg >= npin && pg < used_eff) atomicMax(rx + pg, order_f32(page_x(i)));
+      }
+    }
+    // ... then counts itself in; the last one decides for the request (its loads of req_x
+    // overlap the output combine).  The release of lane 0's counter increment covers the
+    // other lanes' reductions, ordered before it by __syncwarp.
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      last = atom_add_acq_rel_gpu(p.req_ctr + req, 1) == p.n_kv - 1;
+      p.counter[unit] = 0;
+      if (evicting) atomicAdd(p.stats + 2, 1ull);
+      atomicAdd(p.stats + 3, 1ull);
+      if (last) p.req_ctr[req] = 0;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    __syncwarp();  // orders lane 0's acquire before the other lanes' loads of req_x
+    if (last) {
+      rq = true;
+      load_meta(0, used_eff);
+    }
+  }
   // ---- a5 (2): out[h][d] = sum_s w_s acc_s[h][d] / L_h ----
   for (int cb = 0; 32 * cb < nch; cb += CB) {
     float4 o[CB];
@@ -289,19 +351,13 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     }
   }
   // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
-  float lse[MAX_GROUP];
+  if (p.table_scope != 0 && !rq) return;  // another kv-head of the request decides
+  if (rq) {
 #pragma unroll
-  for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
-  // page score x_p = max_h (score_hp - LSE_h) (log2 domain).  Rule 0: stamp iff x_p > log2 a
-  // (strict, D3).  Rule 1 (top-r, PAPER.md :135, reading D23): stamp the k = ceil(r n) pages with
-  // the largest (x_p, -start_pos) among the n unpinned resident pages.
-  auto page_x = [&](int i) {
-    float x = -INFINITY;
-#pragma unroll
-    for (int h = 0; h < MAX_GROUP; ++h)
-      if (h < g) x = fmaxf(x, pmv[i][h] - lse[h]);
-    return x;
-  };
+    for (int h = 0; h < MAX_GROUP; ++h) lse[h] = 0.f;  // req_x already holds normalised scores
+  }
+  const int nrep = p.table_scope != 0 ? p.n_kv : 1;   // metadata replicas this warp writes
+  const int unit0 = p.table_scope != 0 ? req * p.n_kv : unit;
   auto page_key = [&](float x, int st) {  // larger key = ranked first; valid keys are > 0
     const uint32_t b = __float_as_uint(x);
     const uint32_t sx = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -346,12 +402,15 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     for (int i = 0; i < PPL; ++i) {
       const int pg = pc + 32 * i + lane;
       if (pg < used_eff) {
-        const size_t ix = (size_t)unit * C + pg;
         int ts_p = tsv[i], st_p = stv[i];
         const bool is_slot = pg == slot;
         if (is_slot) {
-          if (off == 0) { st_p = t; p.start[ix] = t; }
-          p.cnt[ix] = off + 1;
+          if (off == 0) st_p = t;
+          for (int r = 0; r < nrep; ++r) {
+            const size_t ix = (size_t)(unit0 + r) * C + pg;
+            if (off == 0) p.start[ix] = t;
+            p.cnt[ix] = off + 1;
+          }
         }
         if (pg >= npin) {
           const float x = page_x(i);
@@ -359,7 +418,11 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
                                                : x > p.log2_alpha;  // strict (D3)
           ++n_dec;
           n_stamp += stamp ? 1 : 0;
-          if (stamp || is_slot) { ts_p = t; p.ts[ix] = t; }  // stamp, or write refresh (D8)
+          if (stamp || is_slot) {  // stamp, or write refresh (D8)
+            ts_p = t;
+            for (int r = 0; r < nrep; ++r) p.ts[(size_t)(unit0 + r) * C + pg] = t;
+          }
+          if (rq) rx[pg] = 0u;  // reset for the next step
           cand_update(best, cand_key(ts_p, st_p), pg);
         }
       }
@@ -369,12 +432,15 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
   if (lane == 0) {
-    p.plan[unit] = next_plan(slot, off + 1, used_eff, C, t, victim, p.status);
-    p.counter[unit] = 0;
+    const int4 np = next_plan(slot, off + 1, used_eff, C, t, victim, p.status);
+    for (int r = 0; r < nrep; ++r) p.plan[unit0 + r] = np;
     atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
     atomicAdd(p.stats + 1, (unsigned long long)n_dec);
-    if (evicting) atomicAdd(p.stats + 2, 1ull);
-    atomicAdd(p.stats + 3, 1ull);
+    if (!rq) {
+      p.counter[unit] = 0;
+      if (evicting) atomicAdd(p.stats + 2, 1ull);
+      atomicAdd(p.stats + 3, 1ull);
+    }
   }
 }
 

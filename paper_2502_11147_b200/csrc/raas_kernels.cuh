@@ -52,6 +52,10 @@ struct DecodeParams {
   int quest_k;       // > 0: Quest-on-prefill hybrid (D24), pages selected per step
   const int32_t* nfull;  // [units] full prompt pages (selectable)
   const int32_t* vmap;   // [units][C] selected prompt pages of this step, ascending
+  int table_scope;       // 0 per (request, kv-head) tables; 1 one table per request (D25)
+  int n_kv;              // kv-heads per request (units of one request are consecutive)
+  uint32_t* req_x;       // [batch][C] table_scope 1: order-preserving max of the page scores
+  int32_t* req_ctr;      // [batch]    table_scope 1: kv-heads of the request combined so far
   float scale_log2;  // softmax_scale * log2(e)
   float log2_alpha;  // log2(alpha); -inf for alpha == 0
 };

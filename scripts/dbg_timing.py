@@ -12,12 +12,18 @@ ap.add_argument("--B", type=int, default=64); ap.add_argument("--Hq", type=int, 
 ap.add_argument("--Hkv", type=int, default=8); ap.add_argument("--L", type=int, default=2048)
 ap.add_argument("--P", type=int, default=256); ap.add_argument("--sp", type=int, default=0)
 ap.add_argument("--layers", type=int, default=8)
+ap.add_argument("--table-scope", type=int, default=0)
 a = ap.parse_args()
 B, Hq, Hkv, d, P, L = a.B, a.Hq, a.Hkv, 128, a.P, a.L
 C, Pp, U = L // 16, P // 16, B * Hkv
 Pp = -(-P // 16)
 meta = random_steady_state(77, U, C, Pp, Pp * 16 + 64 * (C - Pp) + 5)
-layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=a.sp) for _ in range(a.layers)]
+if a.table_scope:  # one table per request: replicate kv-head 0's state
+    for k in ("t", "ts", "start", "count", "pinned"):
+        v = meta[k].reshape(B, Hkv, *meta[k].shape[1:])
+        meta[k] = np.ascontiguousarray(np.repeat(v[:, :1], Hkv, axis=1).reshape(meta[k].shape))
+layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=a.sp, table_scope=a.table_scope)
+          for _ in range(a.layers)]
 print(layers[0].raas_launch_info())
 for ly in layers:
     ly.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"])

@@ -10,4 +10,7 @@ st = waterfall_stream(1000, 1, 4, 2, 64, 32, 40)
 r1, _, _ = run_lockstep(oracle, st, L=64, alpha=1e-4, Hq=4, Hkv=2)
 st = waterfall_stream(7, 2, 8, 2, 128, 40, 30)
 r2, _, _ = run_lockstep(oracle, st, L=256, alpha=1e-4, Hq=8, Hkv=2, split_pages=4)
-print("sanitize case ok", r1.max_err, r2.max_err, r1.band_events + r2.band_events)
+st = waterfall_stream(8, 2, 8, 2, 128, 40, 30)
+r3, _, _ = run_lockstep(oracle, st, L=256, alpha=1e-4, Hq=8, Hkv=2, split_pages=4, table_scope=1)
+print("sanitize case ok", r1.max_err, r2.max_err, r3.max_err,
+      r1.band_events + r2.band_events + r3.band_events)

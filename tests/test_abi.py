@@ -71,7 +71,7 @@ def test_arena_bytes(L, cfg, expect):
 @pytest.mark.parametrize("extra", [dict(score_mode=2), dict(stamp_rule=3), dict(stamp_rule=1, top_r=1.5),
                                    dict(quest_prefill_pages=-1), dict(split_pages=33),
                                    dict(stamp_rule=1, top_r=0.5, L=16384),
-                                   dict(quest_prefill_pages=8, L=16384)])
+                                   dict(quest_prefill_pages=8, L=16384), dict(table_scope=2)])
 def test_arena_bytes_rejects_bad_modes(L, extra):
     base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
     base.update(extra)

@@ -487,3 +487,63 @@ def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp
     # selection (the data are seeded, so this holds or fails deterministically)
     assert gaps and min(gaps) > 2e-6, "selection boundary too close for an fp32-vs-fp64 check"
     assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
+
+
+# ------------------------------------------------------------------ NEXT-2: one table per request
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,rule,score,alpha", [
+    (2, 32, 8, 128, 40, 260, 256, 0, 0, 0, 3e-3),   # Llama-3.1-8B heads, 8 replicas per request
+    (2, 28, 4, 128, 64, 200, 192, 4, 0, 0, 2e-3),   # Qwen group of 7, split units
+    (3, 4, 2, 64, 32, 256, 64, 0, 0, 0, 0.03),      # toy shapes
+    (2, 8, 2, 128, 40, 260, 256, 3, 1, 0, 1e-4),    # top-r over the request-wide scores
+    (2, 8, 2, 128, 40, 220, 256, 0, 0, 1, 0.2),     # Quest bound scores
+])
+def test_request_table_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, rule, score, alpha):
+    """table_scope = 1 (reading D25): one page table per request, OR over all its q-heads,
+    GPU vs oracle in lockstep; every kv-head's replica of the state stays identical.  alpha is
+    raised per case: with the OR over up to 32 heads, 1e-4 stamps every page of these streams
+    (the smallest |p* - alpha| of each case is > 1e-6, checked by the band counter)."""
+    st = waterfall_stream(600 + B + Hq + P + rule, B, Hq, Hkv, d, P, T)
+
+    def on_step(i, layer, oracle, g_out, o_out):
+        if i % 25 == 0:
+            s = layer.raas_get_state()
+            for k in ("ts", "start", "count", "pinned"):
+                a = s[k].reshape(B, Hkv, -1)
+                assert (a == a[:, :1]).all(), k
+
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=alpha, Hq=Hq, Hkv=Hkv, split_pages=sp,
+                                 score_mode=score, stamp_rule=rule, table_scope=1, on_step=on_step)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
+    c = layer.raas_get_counters()
+    assert c["unit_steps"] == T * B * Hkv and 0 < c["stamps"] < c["decisions"]
+
+
+def test_request_table_sharding_bitwise_and_set_state_validation():
+    """table_scope = 1: request shards reproduce the unsharded run bitwise; raas_set_state
+    rejects kv-head replicas that disagree."""
+    st = waterfall_stream(31, 4, 8, 2, 128, 48, 150)
+
+    def run(sl=slice(None)):
+        kp, vp = st.k_pre[sl], st.v_pre[sl]
+        layer = RaasLayer(256, 1e-4, 8, 2, 128, kp.shape[0], split_pages=2, table_scope=1)
+        layer.raas_prefill(to_dev(kp), to_dev(vp), kp.shape[2])
+        out = torch.empty((kp.shape[0], 8, 128), dtype=torch.bfloat16, device="cuda")
+        outs = []
+        for i in range(st.T):
+            layer.raas_decode_step(to_dev(st.q[i][sl]), to_dev(st.k[i][sl]), to_dev(st.v[i][sl]), out)
+            outs.append(from_dev(out))
+        return np.stack(outs), layer.raas_get_state(), layer
+
+    a, sa, layer = run()
+    lo, slo, _ = run(slice(0, 2))
+    hi, shi, _ = run(slice(2, 4))
+    assert np.array_equal(np.concatenate([lo, hi], axis=1), a)
+    for k in ("ts", "start", "count"):
+        assert np.array_equal(np.concatenate([slo[k], shi[k]]), sa[k])
+    bad = {k: v.copy() for k, v in sa.items()}
+    bad["ts"][1, -1] += 1   # unit 1 = kv-head 1 of request 0
+    with pytest.raises(RaasError):
+        layer.raas_set_state(bad["t"], bad["ts"], bad["start"], bad["count"], bad["pinned"])
+    layer.raas_set_state(sa["t"], sa["ts"], sa["start"], sa["count"], sa["pinned"])
