@@ -231,7 +231,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     score_mode = 1 if args.score == "quest" else 0
     layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode,
                         stamp_rule=1 if args.top_r > 0 else 0, top_r=args.top_r,
-                        quest_prefill_pages=args.quest_prefill, table_scope=args.table_scope)
+                        quest_prefill_pages=args.quest_prefill, table_scope=args.table_scope,
+                        page=args.page)
               for _ in range(nl)]
     info = layers[0].raas_launch_info()
     for ly in layers:
@@ -277,8 +278,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     step0 = fill_steps
     c0 = [ly.raas_get_counters() for ly in layers]
     st0 = layers[0].raas_get_state()
-    log(f"[rank {rank}] filled {fill_steps} model steps in {t_fill:.1f}s; used pages/unit="
-        f"{(st0['count'] > 0).sum(1).mean():.1f}/{C}; launch {info}")
+    Ce = L // args.page  # state entries per unit: pages, or token slots (page = 1)
+    log(f"[rank {rank}] filled {fill_steps} model steps in {t_fill:.1f}s; used entries/unit="
+        f"{(st0['count'] > 0).sum(1).mean():.1f}/{Ce}; launch {info}")
 
     # warmup
     with torch.cuda.stream(stream):
@@ -318,20 +320,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     # algorithmic bytes per launch: K+V of resident tokens (steady state: the
     # write page holds 1..16 tokens, the others are full -> mean occupancy L-7.5 over a page
     # cycle; exact from the state at the timed steps), new K/V write, q read + out write,
-    # page metadata (ts/start/count) ~12 B per page.
+    # metadata (ts/start/count) <= 12 B per entry (page, or token slot when page = 1).
     st1 = layers[0].raas_get_state()
     occ_now = st1["count"].sum(1).mean()
-    if (st0["count"] > 0).sum(1).min() == C:
-        occ_mean = L - 7.5
+    if (st0["count"] > 0).sum(1).min() == Ce:
+        occ_mean = L - 7.5 if args.page == 16 else float(L)  # token slots: always all L
     else:
         occ_mean = float(occ_now)
     nfull = P // 16
     if args.quest_prefill and nfull > args.quest_prefill:
         # hybrid: only K of the nfull prompt pages are read, plus their representative keys
         occ_mean -= (nfull - args.quest_prefill) * 16
-        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * C + nfull * 4 * d)
+        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce + nfull * 4 * d)
     else:
-        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * C)
+        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce)
     launch_s = ms_per_step / 1e3 / nl
     achieved = bytes_launch / launch_s / 1e9
     peak, peak_src = measured_peaks()
@@ -404,7 +406,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)",
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
                    "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
-                   "page": 16, "alpha": args.alpha, "score_mode": args.score,
+                   "page": args.page, "alpha": args.alpha, "score_mode": args.score,
                    "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
                    "quest_prefill_pages": args.quest_prefill,
                    "table_scope": "request" if args.table_scope else "kv-head",
@@ -494,6 +496,8 @@ def main():
                     help="stamp the top r fraction of pages instead of the alpha threshold (NEXT-3)")
     ap.add_argument("--score", default="exact", choices=["exact", "quest"],
                     help="page score for stamping: exact page max (D4) or Quest bound (NEXT-1)")
+    ap.add_argument("--page", type=int, default=16, choices=[16, 1],
+                    help="1: token-level RaaS (PAPER.md §3.2), one timestamp per token (NEXT-3)")
     ap.add_argument("--table-scope", type=int, default=0, choices=[0, 1],
                     help="1: one page table per request, OR over all heads (reading D25)")
     ap.add_argument("--dense", type=int, default=0,

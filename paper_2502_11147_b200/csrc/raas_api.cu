@@ -58,6 +58,7 @@ struct Layout {
 
 struct Derived {
   int C, units, g, split_pages, nsplit;
+  int Ce, ep;  // metadata entries per unit (L / page) of ep = page tokens; C = L / 16 tiles
 };
 
 int derive(const raas_config* c, Derived* d) {
@@ -73,14 +74,22 @@ int derive(const raas_config* c, Derived* d) {
   if (c->stamp_rule != 0 && c->stamp_rule != 1) return fail(RAAS_E_INVALID, "stamp_rule must be 0 or 1");
   if (c->stamp_rule == 1 && !(c->top_r >= 0.f && c->top_r <= 1.f))
     return fail(RAAS_E_INVALID, "top_r must be in [0, 1]");
-  if (c->page != raas::PAGE) return fail(RAAS_E_UNSUPPORTED, "page must be 16");
+  if (c->page != raas::PAGE && c->page != 1)
+    return fail(RAAS_E_UNSUPPORTED, "page must be 16 (pages) or 1 (token-level RaaS)");
+  if (c->L % raas::PAGE != 0) return fail(RAAS_E_UNSUPPORTED, "L must be a multiple of 16");
+  d->ep = c->page;
+  d->Ce = c->L / c->page;
+  if (c->page == 1 && c->score_mode != 0)
+    return fail(RAAS_E_UNSUPPORTED, "page = 1: the representative-key bound of one key is the key itself; use score_mode 0");
+  if (c->page == 1 && c->quest_prefill_pages > 0)
+    return fail(RAAS_E_UNSUPPORTED, "the Quest-on-prefill hybrid needs page = 16");
   if (c->head_dim != 64 && c->head_dim != 128)
     return fail(RAAS_E_UNSUPPORTED, "head_dim must be 64 or 128");
   d->g = c->n_q_heads / c->n_kv_heads;
   if (d->g > raas::MAX_GROUP) return fail(RAAS_E_UNSUPPORTED, "GQA group > 8");
-  d->C = c->L / c->page;
-  if (c->stamp_rule == 1 && d->C > 512)
-    return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports L <= 8192 (512 pages)");
+  d->C = c->L / raas::PAGE;
+  if (c->stamp_rule == 1 && d->Ce > 512)
+    return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports at most 512 pages (token slots) per unit");
   if (c->quest_prefill_pages < 0) return fail(RAAS_E_INVALID, "quest_prefill_pages must be >= 0");
   if (c->table_scope != 0 && c->table_scope != 1) return fail(RAAS_E_INVALID, "table_scope must be 0 or 1");
   if (c->quest_prefill_pages > 0 && d->C > 512)
@@ -107,9 +116,10 @@ Layout layout(const raas_config* c, const Derived& d) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = up(o + bytes); return r; };
   L.kvstore = take(U * C * 2 * raas::PAGE * D * 2);
-  L.ts = take(U * C * 4);
-  L.start = take(U * C * 4);
-  L.cnt = take(U * C * 4);
+  const size_t Ce = d.Ce;  // metadata entries (pages, or token slots when page = 1)
+  L.ts = take(U * Ce * 4);
+  L.start = take(U * Ce * 4);
+  L.cnt = take(U * Ce * 4);
   L.npin = take(U * 4);
   L.nfull = take(U * 4);
   const bool hyb = c->quest_prefill_pages > 0;  // Quest-on-prefill hybrid workspace (NEXT-4)
@@ -118,9 +128,9 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.plen = take((size_t)c->batch * 4);
   L.plan = take(U * 16);
   L.counter = take(U * 4);
-  L.req_x = c->table_scope ? take((size_t)c->batch * C * 4) : 0;   // zeroed by raas_create
+  L.req_x = c->table_scope ? take((size_t)c->batch * Ce * 4) : 0;   // zeroed by raas_create
   L.req_ctr = c->table_scope ? take((size_t)c->batch * 4) : 0;
-  L.pmax = take(U * C * g * 4);
+  L.pmax = take(U * Ce * g * 4);
   L.part_acc = take(U * d.nsplit * g * D * 4);
   L.part_ml = take(U * d.nsplit * g * 8);
   L.status = take(16);
@@ -219,6 +229,8 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.stats = reinterpret_cast<unsigned long long*>(a + h->lay.stats);
   p.units = h->d.units;
   p.C = h->d.C;
+  p.Ce = h->d.Ce;
+  p.ep = h->d.ep;
   p.nsplit = h->d.nsplit;
   p.split_pages = h->d.split_pages;
   p.g = h->d.g;
@@ -327,7 +339,7 @@ int refresh(raas_handle* h, cudaStream_t st) {
       reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
       reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
       reinterpret_cast<int4*>(a + h->lay.plan), reinterpret_cast<int32_t*>(a + h->lay.counter),
-      reinterpret_cast<uint32_t*>(a + h->lay.status), h->d.units, h->d.C);
+      reinterpret_cast<uint32_t*>(a + h->lay.status), h->d.units, h->d.Ce, h->d.ep);
   RAAS_CUDA(cudaGetLastError());
   return RAAS_OK;
 }
@@ -398,9 +410,10 @@ int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int3
   for (int b = 0; b < B; ++b) {
     if (P_host[b] < 0 || P_host[b] > P_max)
       return fail(RAAS_E_INVALID, "P[%d]=%d outside [0, P_max=%d]", b, P_host[b], P_max);
-    const int Pp = (P_host[b] + raas::PAGE - 1) / raas::PAGE;
-    if (Pp >= h->d.C)
-      return fail(RAAS_E_BUDGET, "request %d: ceil(P/16)=%d leaves no decode page (C=%d)", b, Pp, h->d.C);
+    const int Pp = (P_host[b] + h->d.ep - 1) / h->d.ep;
+    if (Pp >= h->d.Ce)
+      return fail(RAAS_E_BUDGET, "request %d: ceil(P/page)=%d leaves no decode entry (L/page=%d)", b, Pp,
+                  h->d.Ce);
   }
   if (P_max > 0 && (!k || !v || !aligned16(k) || !aligned16(v)))
     return fail(RAAS_E_INVALID, "k/v must be non-null 16-byte aligned device pointers");
@@ -424,12 +437,12 @@ int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int3
           h->d.units, h->cfg.n_kv_heads, P_max, h->d.C);
     RAAS_CUDA(cudaGetLastError());
   }
-  const size_t n = (size_t)h->d.units * h->d.C;
+  const size_t n = (size_t)h->d.units * h->d.Ce;
   raas::raas_meta_init<<<(int)std::min<size_t>((n + 255) / 256, 4096), 256, 0, st>>>(
       reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
       reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
       reinterpret_cast<int32_t*>(a + h->lay.nfull), reinterpret_cast<int4*>(a + h->lay.plan), plen,
-      h->d.units, h->cfg.n_kv_heads, h->d.C);
+      h->d.units, h->cfg.n_kv_heads, h->d.Ce, h->d.ep);
   RAAS_CUDA(cudaGetLastError());
   int rc = build_repkeys(h, st);
   if (!rc) rc = refresh(h, st);
@@ -484,7 +497,7 @@ int raas_get_state(raas_handle* h, int32_t* t, int32_t* ts, int32_t* start_pos, 
   if (!h) return fail(RAAS_E_INVALID, "null handle");
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t U = h->d.units, C = h->d.C;
+  const size_t U = h->d.units, C = h->d.Ce;  // metadata entries (pages, or token slots)
   std::vector<int32_t> npin(U), vts(U * C);
   std::vector<int4> plan(U);
   uint8_t* a = h->arena;
@@ -514,7 +527,7 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   if (!t || !ts || !start_pos || !count || !pinned) return fail(RAAS_E_INVALID, "null state array");
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t U = h->d.units, C = h->d.C;
+  const size_t U = h->d.units, C = h->d.Ce;  // metadata entries (pages, or token slots)
   std::vector<int32_t> npin(U);
   std::vector<int4> plan(U);
   for (size_t u = 0; u < U; ++u) {
@@ -524,7 +537,7 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
       if (pinned[u * C + p]) return fail(RAAS_E_INVALID, "pinned pages must be a prefix (unit %zu)", u);
     bool hole = false;
     for (size_t p = 0; p < C; ++p) {
-      if (count[u * C + p] < 0 || count[u * C + p] > raas::PAGE)
+      if (count[u * C + p] < 0 || count[u * C + p] > h->d.ep)
         return fail(RAAS_E_INVALID, "count out of range");
       if (count[u * C + p] == 0) hole = true;
       else if (hole) return fail(RAAS_E_INVALID, "used pages must be a prefix (unit %zu)", u);
@@ -552,7 +565,7 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   // set_state: the pinned pages are taken as full prompt pages (hybrid selection set)
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.nfull, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.plan, plan.data(), U * 16, cudaMemcpyHostToDevice, st));
-  const size_t pages = U * C, D = h->cfg.head_dim;
+  const size_t pages = U * h->d.C, D = h->cfg.head_dim;  // 16-row tiles
   std::vector<uint16_t> dev;
   if (k_store_host || v_store_host) {
     dev.resize(pages * 2 * raas::PAGE * D);

@@ -185,7 +185,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   // Latency-oriented: the plan, the split statistics, the first block of split partials and
   // the first 128 pages' metadata are all requested before any of them is used (nse comes with
   // the queue entry), so a unit costs ~one dependent L2 round trip before its stores.
-  const int C = p.C, g = p.g;
+  const int C = p.Ce, g = p.g;  // metadata entries: pages, or token slots (ep = 1)
   const int NE = nse * g;
   const uint32_t scr_w = scr;                                   // float[nse][g] split weights
   const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
@@ -432,7 +432,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
   if (lane == 0) {
-    const int4 np = next_plan(slot, off + 1, used_eff, C, t, victim, p.status);
+    const int4 np = next_plan(slot, off + 1, used_eff, C, t, victim, p.status, p.ep);
     for (int r = 0; r < nrep; ++r) p.plan[unit0 + r] = np;
     atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
     atomicAdd(p.stats + 1, (unsigned long long)n_dec);
@@ -511,8 +511,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
   if (threadIdx.x == 0) g_raas_dbg[blockIdx.x][12] = dbg_gtimer();
 #endif
 
-  const int C = p.C, SP = p.split_pages, g = p.g;
+  const int C = p.C, SP = p.split_pages, g = p.g;  // C: 16-row tiles (pages) per unit
   const int n_tiles = p.units * p.nsplit;
+  const bool tok = p.ep == 1;  // token-level RaaS (NEXT-3): metadata per row, tiles physical only
 
   // multi-consumer combine queue: the combine warp from the start, the consumers after END
   auto combine_loop = [&](uint32_t scratch) {
@@ -559,9 +560,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         const int nf = p.quest_k > 0 ? p.nfull[u] : 0;
         const bool hyb = p.quest_k > 0 && nf > p.quest_k;
         const int v = q0 + lane;
-        nnatt = hyb ? p.quest_k + nplan.z - nf : nplan.z;
-        nphys = !hyb ? v : (v < p.quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - p.quest_k));
-        ncnt = (lane < SP && v < nnatt) ? p.cnt[(size_t)u * C + nphys] : 0;
+        if (tok) {  // token slots: used slots are the prefix [0, z), so tile v holds z - 16v rows
+          nnatt = (nplan.z + PAGE - 1) / PAGE;
+          nphys = v;
+          ncnt = (lane < SP && v < nnatt) ? min(PAGE, nplan.z - PAGE * v) : 0;
+        } else {
+          nnatt = hyb ? p.quest_k + nplan.z - nf : nplan.z;
+          nphys = !hyb ? v : (v < p.quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - p.quest_k));
+          ncnt = (lane < SP && v < nnatt) ? p.cnt[(size_t)u * C + nphys] : 0;
+        }
       }
     };
     TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
@@ -618,8 +625,10 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           const uint32_t jj = j + lane;
           const int s = (int)(jj % S);
           RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
-          const bool is_slot = page == slot;
-          sinfo[2 * s] = make_int4(unit, page, is_slot ? off + 1 : c, is_slot ? off : -1);
+          // the tile the new token goes to, its row count and the row it is written to
+          const bool is_slot = tok ? page == (slot >> 4) : page == slot;
+          const int patch = !is_slot ? -1 : (tok ? (slot & (PAGE - 1)) : off);
+          sinfo[2 * s] = make_int4(unit, page, (is_slot && !tok) ? off + 1 : c, patch);
           sinfo[2 * s + 1] =
               make_int4(k, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
           mbar_arrive_expect_tx(full(s), STAGE);
@@ -923,7 +932,17 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         sc0 = __shfl_sync(0xffffffffu, v[0], lane_of(2 * qd)) * p.scale_log2;
         sc1 = __shfl_sync(0xffffffffu, v[0], lane_of(2 * qd + 1)) * p.scale_log2;
       }
-      if (lane < 4) {  // a4: page score per head ("a single attention score per page", :147)
+      if (tok) {  // a4, token level (§3.2): every row's logit per head
+        float* px = p.pmax + ((size_t)(unit * C + page) * PAGE + r) * g;
+        if (r < cnt) {
+          if (2 * qd < g) px[2 * qd] = s0;
+          if (2 * qd + 1 < g) px[2 * qd + 1] = s1;
+        }
+        if (r + 8 < cnt) {
+          if (2 * qd < g) px[8 * g + 2 * qd] = s2;
+          if (2 * qd + 1 < g) px[8 * g + 2 * qd + 1] = s3;
+        }
+      } else if (lane < 4) {  // a4: page score per head ("a single attention score per page", :147)
         float* pmx = p.pmax + (size_t)(unit * C + page) * g;
         if (2 * qd < g) pmx[2 * qd] = sc0;
         if (2 * qd + 1 < g) pmx[2 * qd + 1] = sc1;

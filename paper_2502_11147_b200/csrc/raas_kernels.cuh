@@ -46,6 +46,9 @@ struct DecodeParams {
   uint32_t* status;
   unsigned long long* stats;  // [4]: stamps, decisions, evictions, unit-steps
   int units, C, nsplit, split_pages, g;
+  // metadata entries: Ce = L / ep per unit, ep tokens each (ep = 16: pages, the tiles C = Ce;
+  // ep = 1: token-level RaaS of PAPER.md §3.2 (NEXT-3), slot s = row s % 16 of tile s / 16)
+  int Ce, ep;
   int score_mode;    // 0 exact page max (D4), 1 Quest representative-key bound (D22)
   int stamp_rule;    // 0 threshold alpha (D2/D3), 1 top-r fraction of pages (D23)
   float top_r;
@@ -146,10 +149,11 @@ __device__ __forceinline__ unsigned long long rank_key(float x, uint32_t tie) {
   return (static_cast<unsigned long long>(sx) << 32) | (0xffffffffu - tie);
 }
 
-// plan for the step after one that wrote `off_written` (0-based) into `slot` at time t
+// plan for the step after one that left `cnt_slot` tokens in entry `slot` at time t (entries
+// of ep tokens, Ce of them; used_eff in use): keep filling, open the next entry, or evict
 __device__ __forceinline__ int4 next_plan(int slot, int cnt_slot, int used_eff, int C, int t,
-                                          int victim, uint32_t* status) {
-  if (cnt_slot < PAGE) return make_int4(slot, cnt_slot, used_eff, t + 1);
+                                          int victim, uint32_t* status, int ep) {
+  if (cnt_slot < ep) return make_int4(slot, cnt_slot, used_eff, t + 1);
   if (used_eff < C) return make_int4(used_eff, 0, used_eff + 1, t + 1);
   if (victim < 0) { atomicOr(status, 1u); victim = slot; }
   return make_int4(victim, 1 << 16, used_eff, t + 1);
@@ -192,20 +196,21 @@ __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
 // t = P(u), with P(u) = plen[u / n_kv_heads] (variable prompt lengths, NEXT-2)
 __global__ void raas_meta_init(int32_t* ts, int32_t* start, int32_t* cnt, int32_t* npin,
                                int32_t* nfull, int4* plan, const int32_t* __restrict__ plen,
-                               int units, int n_kv_heads, int C) {
+                               int units, int n_kv_heads, int C, int ep) {
+  // C entries of ep tokens per unit (ep = 16 pages, ep = 1 token slots)
   const size_t total = (size_t)units * C;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int pg = (int)(i % C);
     const size_t u = i / C;
     const int P = plen[u / n_kv_heads];
-    const int Pp = (P + PAGE - 1) / PAGE;
+    const int Pp = (P + ep - 1) / ep;
     ts[i] = 0;
-    start[i] = pg < Pp ? pg * PAGE + 1 : 0;
-    cnt[i] = pg < Pp ? min(PAGE, P - pg * PAGE) : 0;
+    start[i] = pg < Pp ? pg * ep + 1 : 0;
+    cnt[i] = pg < Pp ? min(ep, P - pg * ep) : 0;
     if (pg == 0) {
       npin[u] = Pp;
-      nfull[u] = P / PAGE;  // full prompt pages: selectable by the hybrid mode (D24)
+      nfull[u] = P / ep;  // full prompt pages: selectable by the hybrid mode (D24)
       plan[u] = make_int4(0, 0, 0, P + 1);  // .w = t + 1; the rest derived by raas_refresh
     }
   }
@@ -215,7 +220,7 @@ __global__ void raas_meta_init(int32_t* ts, int32_t* start, int32_t* cnt, int32_
 // One warp per unit.  Reads t from plan[u].w - 1.
 __global__ void raas_refresh(const int32_t* ts, const int32_t* start, const int32_t* cnt,
                              const int32_t* npin, int4* plan, int32_t* counter, uint32_t* status,
-                             int units, int C) {
+                             int units, int C, int ep) {
   const int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (unit >= units) return;
@@ -247,7 +252,7 @@ __global__ void raas_refresh(const int32_t* ts, const int32_t* start, const int3
       pl = make_int4(0, 0, 1, t + 1);  // nothing resident yet (P == 0): open page 0
     } else {
       const int cur = (int)(cur_key & 0xffffffffu) - 1;
-      pl = next_plan(cur, cnt[(size_t)unit * C + cur], used, C, t, victim, status);
+      pl = next_plan(cur, cnt[(size_t)unit * C + cur], used, C, t, victim, status, ep);
     }
     plan[unit] = pl;
     counter[unit] = 0;

@@ -138,10 +138,11 @@ class RaasLayer:
 
     def __init__(self, L, alpha, n_q_heads, n_kv_heads, head_dim, batch, device=None,
                  softmax_scale=0.0, split_pages=0, score_mode=SCORE_EXACT,
-                 stamp_rule=STAMP_ALPHA, top_r=0.5, quest_prefill_pages=0, table_scope=0):
+                 stamp_rule=STAMP_ALPHA, top_r=0.5, quest_prefill_pages=0, table_scope=0,
+                 page=16):
         import torch
 
-        self.cfg = make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch,
+        self.cfg = make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch, page=page,
                                softmax_scale=softmax_scale, split_pages=split_pages,
                                score_mode=score_mode, stamp_rule=stamp_rule, top_r=top_r,
                                quest_prefill_pages=quest_prefill_pages, table_scope=table_scope)
@@ -160,7 +161,8 @@ class RaasLayer:
         _check(lib().raas_create(ctypes.byref(self.cfg), ctypes.c_void_p(self.arena_ptr),
                                  nbytes, dev_index, ctypes.byref(h)), "raas_create")
         self._h = h
-        self.L, self.C = L, L // 16
+        # state arrays have one entry per page (page = 16) or per token slot (page = 1)
+        self.L, self.page, self.C = L, page, L // page
         self.hq, self.hkv, self.d, self.batch = n_q_heads, n_kv_heads, head_dim, batch
         self.units = batch * n_kv_heads
 
@@ -211,7 +213,7 @@ class RaasLayer:
                                     _np_ptr(vs), _stream_ptr(stream)), "raas_set_state")
 
     def raas_get_kv(self, stream=None):
-        shape = (self.units, self.C, 16, self.d)
+        shape = (self.units, self.C, self.page, self.d)
         k = np.zeros(shape, np.uint16)
         v = np.zeros(shape, np.uint16)
         _check(lib().raas_get_kv(self._h, _np_ptr(k), _np_ptr(v), _stream_ptr(stream)), "raas_get_kv")

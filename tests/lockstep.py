@@ -70,16 +70,17 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None):
 
 def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_every=1,
                  layer=None, oracle=None, device="cuda", on_step=None, score_mode=0,
-                 stamp_rule=0, top_r=0.5, quest_prefill_pages=0, table_scope=0):
+                 stamp_rule=0, top_r=0.5, quest_prefill_pages=0, table_scope=0, page=16):
     """Drive both sides through the whole stream; returns LockstepResult."""
     B, _, P, d = stream.k_pre.shape
     if layer is None:
         layer = RaasLayer(L, alpha, Hq, Hkv, d, B, device=device, split_pages=split_pages,
                           score_mode=score_mode, stamp_rule=stamp_rule, top_r=top_r,
-                          quest_prefill_pages=quest_prefill_pages, table_scope=table_scope)
+                          quest_prefill_pages=quest_prefill_pages, table_scope=table_scope,
+                          page=page)
         layer.raas_prefill(to_dev(stream.k_pre, device), to_dev(stream.v_pre, device), P)
     if oracle is None:
-        oracle = oracle_mod.Oracle(L=L, alpha=alpha, page=16, n_q_heads=Hq, n_kv_heads=Hkv,
+        oracle = oracle_mod.Oracle(L=L, alpha=alpha, page=page, n_q_heads=Hq, n_kv_heads=Hkv,
                                    head_dim=d, batch=B, score_mode=score_mode,
                                    stamp_rule=stamp_rule, top_r=top_r,
                                    quest_prefill_pages=quest_prefill_pages, table_scope=table_scope)

@@ -71,7 +71,10 @@ def test_arena_bytes(L, cfg, expect):
 @pytest.mark.parametrize("extra", [dict(score_mode=2), dict(stamp_rule=3), dict(stamp_rule=1, top_r=1.5),
                                    dict(quest_prefill_pages=-1), dict(split_pages=33),
                                    dict(stamp_rule=1, top_r=0.5, L=16384),
-                                   dict(quest_prefill_pages=8, L=16384), dict(table_scope=2)])
+                                   dict(quest_prefill_pages=8, L=16384), dict(table_scope=2),
+                                   dict(page=8), dict(page=1, L=2040), dict(page=1, score_mode=1),
+                                   dict(page=1, quest_prefill_pages=4),
+                                   dict(page=1, stamp_rule=1, L=1024)])
 def test_arena_bytes_rejects_bad_modes(L, extra):
     base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
     base.update(extra)
@@ -84,6 +87,17 @@ def test_hybrid_mode_adds_representative_keys_only(L):
     a1 = raas.raas_arena_bytes(raas.make_config(**base, quest_prefill_pages=16))
     kv = 2 * 16 * 128 * 2 * 2 * 128 * 16   # units x pages x (K+V rows) bytes
     assert 0 < a1 - a0 <= kv / 16 + 2 * 16 * 128 * 4 + 4096   # min/max keys (1/16 of K) + vmap
+
+
+def test_token_level_arena(L):
+    """page = 1: same KV store, metadata and score rows per token instead of per page."""
+    base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
+    a16 = raas.raas_arena_bytes(raas.make_config(**base))
+    a1 = raas.raas_arena_bytes(raas.make_config(**base, page=1))
+    units, extra_entries = 16, 2048 - 128
+    assert a1 - a16 >= units * extra_entries * (3 * 4 + 4 * 4)   # ts/start/cnt + 4 head scores
+    assert a1 - a16 <= units * extra_entries * (3 * 4 + 4 * 4) + 64 * 1024
+    assert raas.raas_arena_bytes(raas.make_config(**dict(base, page=1, stamp_rule=1, L=512))) > 0
 
 
 def test_arena_is_linear_in_L_not_N(L):

@@ -547,3 +547,40 @@ def test_request_table_sharding_bitwise_and_set_state_validation():
     with pytest.raises(RaasError):
         layer.raas_set_state(bad["t"], bad["ts"], bad["start"], bad["count"], bad["pinned"])
     layer.raas_set_state(sa["t"], sa["ts"], sa["start"], sa["count"], sa["pinned"])
+
+
+# ------------------------------------------------------------------ NEXT-3: token-level RaaS (page = 1)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,rule,scope", [
+    (1, 4, 2, 64, 32, 256, 64, 0, 0, 0),        # toy shapes, token slots
+    (2, 32, 8, 128, 40, 300, 256, 0, 0, 0),     # Llama-3.1-8B heads
+    (2, 28, 4, 128, 37, 260, 192, 3, 0, 0),     # Qwen group, ragged prompt, 3-tile splits
+    (2, 8, 2, 128, 0, 200, 128, 2, 0, 0),       # no prompt (D21)
+    (2, 8, 2, 128, 40, 260, 256, 4, 1, 0),      # top-r over tokens (r = 0.5, :135)
+    (2, 8, 2, 128, 40, 260, 256, 0, 0, 1),      # one table per request
+])
+def test_token_level_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, rule, scope):
+    """page = 1 (§3.2 :98-100, Fig 5): every token is its own entry with its own
+    timestamp; GPU vs oracle, bit-exact state (per token), out within 2e-2."""
+    st = waterfall_stream(700 + B + Hq + P + rule + scope, B, Hq, Hkv, d, P, T)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-3, Hq=Hq, Hkv=Hkv, split_pages=sp,
+                                 stamp_rule=rule, table_scope=scope, page=1)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
+    c = layer.raas_get_counters()
+    assert 0 < c["stamps"] < c["decisions"]
+
+
+@pytest.mark.parametrize("alpha", [0.0, 1.0])
+def test_token_level_alpha_extremes(oracle_mod, alpha):
+    """page = 1, alpha in {0, 1}: token-level sliding window + attention sink (P4 closed form
+    at page = 1): the resident positions are the prompt plus the last L - P tokens."""
+    B, Hq, Hkv, d, P, T, L = 2, 8, 2, 128, 24, 150, 96
+    st = gaussian_stream(31, B, Hq, Hkv, d, P, T)
+    res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=alpha, Hq=Hq, Hkv=Hkv, page=1)
+    s = layer.raas_get_state()
+    t = P + T
+    want = set(range(1, P + 1)) | set(range(t - (L - P) + 1, t + 1))
+    for u in range(B * Hkv):
+        assert set(s["start"][u][s["count"][u] > 0].tolist()) == want
+    assert res.max_err <= OUT_TOL
