@@ -46,19 +46,22 @@ size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 #endif
 constexpr int NC = RAAS_NC;  // consumer (MMA) warps per CTA
 constexpr int S = RAAS_S;    // K+V page stages in the ring (8 KiB each at head_dim 128)
-template <int D>
-using Lay = raas::DecodeLayout<D, NC, S>;
-template <int D>
-constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S>; }
+template <int D, bool TOKD = false>
+using Lay = raas::DecodeLayout<D, NC, S, TOKD>;
+template <int D, bool TOKD>
+constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD>; }
 
 struct Layout {
-  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, req_x, req_ctr, pmax, part_acc, part_ml, status, sched,
+  size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, req_x, req_ctr,
+      q_prev, lse_prev, part_key, pmax, part_acc, part_ml, status, sched,
       stats, sq, sk, sv, so, total;
 };
 
 struct Derived {
   int C, units, g, split_pages, nsplit;
   int Ce, ep;  // metadata entries per unit (L / page) of ep = page tokens; C = L / 16 tiles
+  int tokd;    // token level with deferred stamping (page 1, threshold rule, per-head tables)
+  int pstr;    // bf16 elements per KV page: 2 * 16 * D, + 64 (ts/start trailer) when tokd
 };
 
 int derive(const raas_config* c, Derived* d) {
@@ -79,6 +82,8 @@ int derive(const raas_config* c, Derived* d) {
   if (c->L % raas::PAGE != 0) return fail(RAAS_E_UNSUPPORTED, "L must be a multiple of 16");
   d->ep = c->page;
   d->Ce = c->L / c->page;
+  d->tokd = c->page == 1 && c->stamp_rule == 0 && c->table_scope == 0 && c->score_mode == 0;
+  d->pstr = 2 * raas::PAGE * c->head_dim + (d->tokd ? 64 : 0);
   if (c->page == 1 && c->score_mode != 0)
     return fail(RAAS_E_UNSUPPORTED, "page = 1: the representative-key bound of one key is the key itself; use score_mode 0");
   if (c->page == 1 && c->quest_prefill_pages > 0)
@@ -115,7 +120,7 @@ Layout layout(const raas_config* c, const Derived& d) {
   const size_t U = d.units, C = d.C, D = c->head_dim, g = d.g;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = up(o + bytes); return r; };
-  L.kvstore = take(U * C * 2 * raas::PAGE * D * 2);
+  L.kvstore = take(U * C * d.pstr * 2);
   const size_t Ce = d.Ce;  // metadata entries (pages, or token slots when page = 1)
   L.ts = take(U * Ce * 4);
   L.start = take(U * Ce * 4);
@@ -130,7 +135,11 @@ Layout layout(const raas_config* c, const Derived& d) {
   L.counter = take(U * 4);
   L.req_x = c->table_scope ? take((size_t)c->batch * Ce * 4) : 0;   // zeroed by raas_create
   L.req_ctr = c->table_scope ? take((size_t)c->batch * 4) : 0;
-  L.pmax = take(U * Ce * g * 4);
+  // per-row scores only for the non-deferred token path; pages keep one score per page
+  L.pmax = take(d.tokd ? 16 : U * Ce * g * 4);
+  L.q_prev = d.tokd ? take(U * g * D * 2) : 0;
+  L.lse_prev = d.tokd ? take(U * 8 * 4) : 0;
+  L.part_key = d.tokd ? take(U * d.nsplit * 16) : 0;
   L.part_acc = take(U * d.nsplit * g * D * 4);
   L.part_ml = take(U * d.nsplit * g * 8);
   L.status = take(16);
@@ -161,7 +170,8 @@ struct DeviceGuard {
 // K rows then the 16 V rows, each row keeping its 16-byte chunk c at chunk c ^ (row & 7) (see
 // raas_kernels.cuh).  pack: logical -> device (k or v may be null: that half is left as is);
 // unpack: device -> logical.
-void pack_store(const uint16_t* k, const uint16_t* v, uint16_t* dev, size_t pages, int D) {
+// (pstr: bf16 elements per device page, 2 * 16 * D plus the tokd trailer)
+void pack_store(const uint16_t* k, const uint16_t* v, uint16_t* dev, size_t pages, int D, size_t pstr) {
   const int nch = D / 8;
   for (size_t pg = 0; pg < pages; ++pg)
     for (int half = 0; half < 2; ++half) {
@@ -169,19 +179,19 @@ void pack_store(const uint16_t* k, const uint16_t* v, uint16_t* dev, size_t page
       if (!src) continue;
       for (int r = 0; r < raas::PAGE; ++r) {
         const uint16_t* srow = src + (pg * raas::PAGE + r) * D;
-        uint16_t* drow = dev + ((pg * 2 + half) * raas::PAGE + r) * D;
+        uint16_t* drow = dev + pg * pstr + (half * raas::PAGE + r) * D;
         for (int c = 0; c < nch; ++c) std::memcpy(drow + (c ^ (r & 7)) * 8, srow + c * 8, 16);
       }
     }
 }
-void unpack_store(const uint16_t* dev, uint16_t* k, uint16_t* v, size_t pages, int D) {
+void unpack_store(const uint16_t* dev, uint16_t* k, uint16_t* v, size_t pages, int D, size_t pstr) {
   const int nch = D / 8;
   for (size_t pg = 0; pg < pages; ++pg)
     for (int half = 0; half < 2; ++half) {
       uint16_t* dst = half ? v : k;
       if (!dst) continue;
       for (int r = 0; r < raas::PAGE; ++r) {
-        const uint16_t* srow = dev + ((pg * 2 + half) * raas::PAGE + r) * D;
+        const uint16_t* srow = dev + pg * pstr + (half * raas::PAGE + r) * D;
         uint16_t* drow = dst + (pg * raas::PAGE + r) * D;
         for (int c = 0; c < nch; ++c) std::memcpy(drow + c * 8, srow + (c ^ (r & 7)) * 8, 16);
       }
@@ -231,6 +241,11 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.C = h->d.C;
   p.Ce = h->d.Ce;
   p.ep = h->d.ep;
+  p.tokd = h->d.tokd;
+  p.pstr = h->d.pstr;
+  p.q_prev = h->d.tokd ? reinterpret_cast<__nv_bfloat16*>(a + h->lay.q_prev) : nullptr;
+  p.lse_prev = h->d.tokd ? reinterpret_cast<float*>(a + h->lay.lse_prev) : nullptr;
+  p.part_key = h->d.tokd ? reinterpret_cast<int4*>(a + h->lay.part_key) : nullptr;
   p.nsplit = h->d.nsplit;
   p.split_pages = h->d.split_pages;
   p.g = h->d.g;
@@ -267,7 +282,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(h->grid);
-  lc.blockDim = dim3(Lay<D>::THREADS);
+  lc.blockDim = dim3(Lay<D>::THREADS);  // the same for both instantiations
   lc.dynamicSmemBytes = h->smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
@@ -275,7 +290,8 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D>(), p));
+  if (h->d.tokd) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true>(), p));
+  else           RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false>(), p));
   return RAAS_OK;
 }
 
@@ -304,16 +320,20 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
   return best;
 }
 
-template <int D>
-int setup_kernel(raas_handle* h) {
-  auto k = decode_kernel<D>();
-  h->smem = Lay<D>::SMEM;
+template <int D, bool TOKD>
+int setup_kernel_t(raas_handle* h) {
+  auto k = decode_kernel<D, TOKD>();
+  h->smem = Lay<D, TOKD>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
-  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D>::THREADS, h->smem));
+  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
   h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
   return RAAS_OK;
+}
+template <int D>
+int setup_kernel(raas_handle* h) {
+  return h->d.tokd ? setup_kernel_t<D, true>(h) : setup_kernel_t<D, false>(h);
 }
 
 int build_repkeys(raas_handle* h, cudaStream_t st) {
@@ -339,7 +359,45 @@ int refresh(raas_handle* h, cudaStream_t st) {
       reinterpret_cast<int32_t*>(a + h->lay.ts), reinterpret_cast<int32_t*>(a + h->lay.start),
       reinterpret_cast<int32_t*>(a + h->lay.cnt), reinterpret_cast<int32_t*>(a + h->lay.npin),
       reinterpret_cast<int4*>(a + h->lay.plan), reinterpret_cast<int32_t*>(a + h->lay.counter),
-      reinterpret_cast<uint32_t*>(a + h->lay.status), h->d.units, h->d.Ce, h->d.ep);
+      reinterpret_cast<uint32_t*>(a + h->lay.status), h->d.units, h->d.Ce, h->d.ep, h->d.tokd);
+  RAAS_CUDA(cudaGetLastError());
+  return RAAS_OK;
+}
+
+// tokd: mirror the ts / start arrays into the pages' trailers (the decode kernel reads them
+// with the page)
+int tok_sync(raas_handle* h, cudaStream_t st) {
+  if (!h->d.tokd) return RAAS_OK;
+  uint8_t* a = h->arena;
+  const size_t tiles = (size_t)h->d.units * h->d.C;
+  const int blocks = (int)std::min<size_t>((tiles * 32 + 255) / 256, (size_t)h->num_sms * 8);
+  raas::raas_tok_trailer_sync<<<blocks, 256, 0, st>>>(
+      reinterpret_cast<__nv_bfloat16*>(a + h->lay.kvstore), reinterpret_cast<const int32_t*>(a + h->lay.ts),
+      reinterpret_cast<const int32_t*>(a + h->lay.start), tiles, h->d.pstr);
+  RAAS_CUDA(cudaGetLastError());
+  return RAAS_OK;
+}
+
+// tokd: apply the stamp decisions still pending from the last step (before a state readout)
+int tok_flush(raas_handle* h, cudaStream_t st) {
+  if (!h->d.tokd || !h->prefilled) return RAAS_OK;
+  uint8_t* a = h->arena;
+  const float scale = h->cfg.softmax_scale > 0.f ? h->cfg.softmax_scale
+                                                 : 1.0f / sqrtf((float)h->cfg.head_dim);
+  const float l2a = h->cfg.alpha > 0.f ? log2f(h->cfg.alpha) : -INFINITY;
+  auto* kvs = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kvstore);
+  auto* qp = reinterpret_cast<const __nv_bfloat16*>(a + h->lay.q_prev);
+  auto* lp = reinterpret_cast<const float*>(a + h->lay.lse_prev);
+  auto* ts = reinterpret_cast<int32_t*>(a + h->lay.ts);
+  auto* np = reinterpret_cast<const int32_t*>(a + h->lay.npin);
+  auto* pl = reinterpret_cast<int4*>(a + h->lay.plan);
+  auto* stats = reinterpret_cast<unsigned long long*>(a + h->lay.stats);
+  if (h->cfg.head_dim == 128)
+    raas::raas_tok_flush<128><<<h->d.units, 256, 0, st>>>(kvs, qp, lp, ts, np, pl, stats, h->d.Ce,
+                                                          h->d.g, scale * 1.4426950408889634f, l2a, h->d.pstr);
+  else
+    raas::raas_tok_flush<64><<<h->d.units, 256, 0, st>>>(kvs, qp, lp, ts, np, pl, stats, h->d.Ce,
+                                                         h->d.g, scale * 1.4426950408889634f, l2a, h->d.pstr);
   RAAS_CUDA(cudaGetLastError());
   return RAAS_OK;
 }
@@ -430,11 +488,11 @@ int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int3
     if (h->cfg.head_dim == 128)
       raas::raas_prefill_copy<128><<<blocks, 256, 0, st>>>(
           static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs, plen,
-          h->d.units, h->cfg.n_kv_heads, P_max, h->d.C);
+          h->d.units, h->cfg.n_kv_heads, P_max, h->d.C, h->d.pstr);
     else
       raas::raas_prefill_copy<64><<<blocks, 256, 0, st>>>(
           static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), kvs, plen,
-          h->d.units, h->cfg.n_kv_heads, P_max, h->d.C);
+          h->d.units, h->cfg.n_kv_heads, P_max, h->d.C, h->d.pstr);
     RAAS_CUDA(cudaGetLastError());
   }
   const size_t n = (size_t)h->d.units * h->d.Ce;
@@ -446,6 +504,7 @@ int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int3
   RAAS_CUDA(cudaGetLastError());
   int rc = build_repkeys(h, st);
   if (!rc) rc = refresh(h, st);
+  if (!rc) rc = tok_sync(h, st);
   if (rc) return rc;
   h->prefilled = 1;
   return RAAS_OK;
@@ -498,6 +557,7 @@ int raas_get_state(raas_handle* h, int32_t* t, int32_t* ts, int32_t* start_pos, 
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t U = h->d.units, C = h->d.Ce;  // metadata entries (pages, or token slots)
+  if (int rc = tok_flush(h, st)) return rc;
   std::vector<int32_t> npin(U), vts(U * C);
   std::vector<int4> plan(U);
   uint8_t* a = h->arena;
@@ -568,17 +628,18 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   const size_t pages = U * h->d.C, D = h->cfg.head_dim;  // 16-row tiles
   std::vector<uint16_t> dev;
   if (k_store_host || v_store_host) {
-    dev.resize(pages * 2 * raas::PAGE * D);
+    dev.resize(pages * h->d.pstr);
     if (!k_store_host || !v_store_host) {  // keep the half that is not replaced
       RAAS_CUDA(cudaMemcpyAsync(dev.data(), a + h->lay.kvstore, dev.size() * 2, cudaMemcpyDeviceToHost, st));
       RAAS_CUDA(cudaStreamSynchronize(st));
     }
     pack_store(static_cast<const uint16_t*>(k_store_host), static_cast<const uint16_t*>(v_store_host),
-               dev.data(), pages, (int)D);
+               dev.data(), pages, (int)D, h->d.pstr);
     RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kvstore, dev.data(), dev.size() * 2, cudaMemcpyHostToDevice, st));
   }
   int rc = build_repkeys(h, st);
   if (!rc) rc = refresh(h, st);
+  if (!rc) rc = tok_sync(h, st);
   if (rc) return rc;
   RAAS_CUDA(cudaStreamSynchronize(st));
   h->prefilled = 1;
@@ -590,11 +651,11 @@ int raas_get_kv(raas_handle* h, void* k_store_host, void* v_store_host, void* st
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t pages = (size_t)h->d.units * h->d.C;
-  std::vector<uint16_t> dev(pages * 2 * raas::PAGE * h->cfg.head_dim);
+  std::vector<uint16_t> dev(pages * h->d.pstr);
   RAAS_CUDA(cudaMemcpyAsync(dev.data(), h->arena + h->lay.kvstore, dev.size() * 2, cudaMemcpyDeviceToHost, st));
   RAAS_CUDA(cudaStreamSynchronize(st));
   unpack_store(dev.data(), static_cast<uint16_t*>(k_store_host), static_cast<uint16_t*>(v_store_host),
-               pages, h->cfg.head_dim);
+               pages, h->cfg.head_dim, h->d.pstr);
   return RAAS_OK;
 }
 
@@ -613,11 +674,17 @@ int raas_get_counters(raas_handle* h, uint64_t counters[4], void* stream) {
   if (!h || !counters) return fail(RAAS_E_INVALID, "null argument");
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = tok_flush(h, st)) return rc;
   RAAS_CUDA(cudaMemcpyAsync(counters, h->arena + h->lay.stats, 32, cudaMemcpyDeviceToHost, st));
   RAAS_CUDA(cudaStreamSynchronize(st));
   return RAAS_OK;
 }
 
+#ifdef RAAS_DBG_TOKD_GLOBAL
+RAAS_API int raas_debug_tokd(int32_t* out16) {
+  return cudaMemcpyFromSymbol(out16, raas::g_tokd_dbg, 64) == cudaSuccess ? 0 : 1;
+}
+#endif
 int raas_launch_info(const raas_handle* h, int32_t info[5]) {
   if (!h || !info) return fail(RAAS_E_INVALID, "null argument");
   info[0] = h->grid;

@@ -145,11 +145,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
-template <int D, int NC, int S>
+template <int D, int NC, int S, bool TOKD = false>
 struct DecodeLayout {
   static constexpr int KS = D / 16;
   static constexpr int TILE = PAGE * D * 2;  // one K (or V) page
-  static constexpr int STAGE = 2 * TILE;
+  static constexpr int STAGE = 2 * TILE + (TOKD ? 128 : 0);  // tokd: + the ts/start trailer
   static constexpr int QBUF = MAX_GROUP * D * 2;
   static constexpr int FRAG = KS * 4 + 4;  // floats per lane in a consumer's deposit
   static constexpr int DEPOSIT = FRAG * 32 * 4;
@@ -157,12 +157,18 @@ struct DecodeLayout {
   static constexpr int OFF_Q = OFF_RING + S * STAGE;
   static constexpr int OFF_MERGE = OFF_Q + 2 * QBUF;
   static constexpr int OFF_SCR = OFF_MERGE + 2 * NC * DEPOSIT;            // combine scratch
-  static constexpr int SCR = MAX_SPLITS * MAX_GROUP * 8 + 2 * MAX_GROUP * 4;
+  static constexpr int SCR = MAX_SPLITS * MAX_GROUP * 8 + 6 * MAX_GROUP * 4;
   static constexpr int OFF_SINFO = OFF_SCR + SCR;                          // int4[2] per stage
-  static constexpr int OFF_TINFO = OFF_SINFO + S * 32;                     // int4[2] per parity
+  static constexpr int OFF_TINFO = OFF_SINFO + S * 32;                     // int4[3] per parity
   static constexpr int CQ = 16;                                            // combine queue
-  static constexpr int OFF_CQ = OFF_TINFO + 2 * 32;  // int[CQ] unit ids, then the pop counter
-  static constexpr int OFF_BAR = OFF_CQ + CQ * 4 + 32;
+  static constexpr int OFF_CQ = OFF_TINFO + 2 * 48;  // int[CQ] unit ids, then the pop counter
+  // deferred token level (tokd): per stage the tile's 16 ts + 16 start values; per parity the
+  // previous step's q and LSE; per (parity, consumer) the tile's victim candidate
+  static constexpr int OFF_TSB = (OFF_CQ + CQ * 4 + 32 + 127) / 128 * 128;
+  static constexpr int OFF_CAND = OFF_TSB;
+  static constexpr int OFF_QP = OFF_CAND + (TOKD ? 2 * NC * 16 : 0);
+  static constexpr int QPBUF = QBUF + 32;  // q_prev rows, then 8 floats of LSE
+  static constexpr int OFF_BAR = (OFF_QP + (TOKD ? 2 * QPBUF : 0) + 127) / 128 * 128;
   // After its END sentinel a consumer's two ring stages (w, w+NC) are never written again, so
   // for D = 128 it joins the combine pool with stage w as its scratch (the kernel's tail is
   // the combines of the last units: more poppers, shorter tail).
@@ -444,11 +450,179 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   }
 }
 
-template <int D, int NC, int S>
-__global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
+
+// ---------------------------------------------------------------------------------------------
+// Deferred token-level combine (tokd; NEXT-3): the pass attended the resident rows [0, used)
+// and took step t-1's stamp decisions.  Here: victim = min over the splits' candidates (if the
+// cache is full), out = softmax over (resident - victim + new token), LSE_t and q_t stored for
+// the next pass's decisions, the new token written into its slot.  PAPER.md §3.2 :98-100.
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit, int nse,
+                                                 uint32_t scr, int lane) {
+  const int C = p.Ce, g = p.g;
+  const int NE = nse * g;
+  const uint32_t scr_w = scr;                                   // float2[nse][g] (m, l) -> w
+  const uint32_t scr_h = scr + MAX_SPLITS * MAX_GROUP * 8;      // per head: M, L, wv, f, wn, inv
+  auto hs = [&](int k, int h) { return scr_h + 4 * (k * MAX_GROUP + h); };
+  const float2* ml_g = p.part_ml + (size_t)unit * p.nsplit * g;
+  const int4 pl = __ldcg(p.plan + unit);  // {fill slot or -1, pending, used rows, t}
+  const int used = pl.z, t = pl.w;
+  const bool evict = used >= C;
+  // split statistics and victim candidates
+  for (int i = lane; i < NE; i += 32) {
+    const float2 ml = __ldcg(ml_g + i);
+    sts_f32(scr_w + 8 * i, ml.x);
+    sts_f32(scr_w + 8 * i + 4, ml.y);
+  }
+  unsigned long long best = ~0ull;
+  int vslot = -1;
+  for (int i = lane; i < nse; i += 32) {
+    const int4 c = __ldcg(p.part_key + (size_t)unit * p.nsplit + i);
+    const unsigned long long key = (static_cast<unsigned long long>(static_cast<uint32_t>(c.y)) << 32) |
+                                   static_cast<uint32_t>(c.x);
+    if (key < best) { best = key; vslot = c.z; }
+  }
+  {
+    const unsigned long long m = warp_min_u64(best);
+    const unsigned hit = __ballot_sync(0xffffffffu, best == m);
+    vslot = __shfl_sync(0xffffffffu, vslot, __ffs(hit) - 1);
+    if (m == ~0ull) vslot = -1;
+  }
+  int slot = used;
+  if (evict) {
+    slot = vslot;
+    if (slot < 0) {  // no unpinned resident row (cannot happen when P < L)
+      if (lane == 0) atomicOr(p.status, 1u);
+      slot = C - 1;
+    }
+  }
+  // this lane's channels: q (all heads), the new K row, the victim's K row (swizzled store)
+  constexpr int CPL = D / 32;                 // channels per lane
+  const int c0 = lane * CPL;
+  const int tile = slot >> 4, row = slot & (PAGE - 1);
+  __nv_bfloat16* const pg0 = p.kvstore + (size_t)(unit * p.C + tile) * p.pstr;
+  const __nv_bfloat16* krow = pg0 + row * D;
+  const __nv_bfloat16* vrow = krow + PAGE * D;
+  auto swz = [&](int c) { return (((c >> 3) ^ (row & 7)) << 3) | (c & 7); };
+  float kn[CPL], kv[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    kn[i] = __bfloat162float(p.k_new[(size_t)unit * D + c0 + i]);
+    kv[i] = evict ? __bfloat162float(krow[swz(c0 + i)]) : 0.f;
+  }
+  float sn[MAX_GROUP], sv[MAX_GROUP];
+#pragma unroll
+  for (int h = 0; h < MAX_GROUP; ++h) {
+    float a = 0.f, b = 0.f;
+    if (h < g) {
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        const float qv = __bfloat162float(p.q[((size_t)unit * g + h) * D + c0 + i]);
+        a += qv * kn[i];
+        b += qv * kv[i];
+      }
+    }
+    sn[h] = warp_sum(a) * p.scale_log2;
+    sv[h] = warp_sum(b) * p.scale_log2;
+  }
+  __syncwarp();
+  if (lane < g) {  // LSE over the splits (reference 0 when no row was resident)
+    float M = -INFINITY;
+    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_w + 8 * (s * g + lane)));
+    const float Mr = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    for (int s = 0; s < nse; ++s) {
+      const uint32_t a = scr_w + 8 * (s * g + lane);
+      const float w = fast_exp2(lds_f32(a) - Mr);
+      L += w * lds_f32(a + 4);
+      sts_f32(a, w);
+    }
+    float s_n = sn[0], s_v = sv[0];
+#pragma unroll
+    for (int h = 1; h < MAX_GROUP; ++h)
+      if (h == lane) { s_n = sn[h]; s_v = sv[h]; }
+    // minus the victim's row, plus the new token (D9: evict -> write -> attend)
+    const float wv = evict ? fast_exp2(s_v - Mr) : 0.f;
+    const float M2 = fmaxf(M, s_n);
+    const float f = M == -INFINITY ? 0.f : fast_exp2(Mr - M2);
+    const float wn = fast_exp2(s_n - M2);
+    const float L2 = fmaxf(L - wv, 0.f) * f + wn;
+    sts_f32(hs(2, lane), wv);
+    sts_f32(hs(3, lane), f);
+    sts_f32(hs(4, lane), wn);
+    sts_f32(hs(5, lane), 1.f / L2);
+    p.lse_prev[(size_t)unit * 8 + lane] = M2 + log2f(L2);  // LSE_t, for the next pass
+  }
+  __syncwarp();
+  // out[h][d] = ((sum_s w_s acc_s - wv v_victim) f + wn v_new) / L'
+  constexpr int CPH = D / 4;
+  const int nch = g * CPH;
+  const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
+  for (int c = lane; c < nch; c += 32) {
+    const int h = c / CPH, d4 = c - h * CPH;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s2 = 0; s2 < nse; ++s2) {
+      const float w = lds_f32(scr_w + 8 * (s2 * g + h));
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)s2 * g + h) * D) + d4);
+      o.x += w * a.x; o.y += w * a.y; o.z += w * a.z; o.w += w * a.w;
+    }
+    const float wv = lds_f32(hs(2, h)), f = lds_f32(hs(3, h)), wn = lds_f32(hs(4, h));
+    const float inv = lds_f32(hs(5, h));
+    float vv[4], vn[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      vv[i] = evict ? __bfloat162float(vrow[swz(4 * d4 + i)]) : 0.f;
+      vn[i] = __bfloat162float(p.v_new[(size_t)unit * D + 4 * d4 + i]);
+    }
+    o.x = ((o.x - wv * vv[0]) * f + wn * vn[0]) * inv;
+    o.y = ((o.y - wv * vv[1]) * f + wn * vn[1]) * inv;
+    o.z = ((o.z - wv * vv[2]) * f + wn * vn[2]) * inv;
+    o.w = ((o.w - wv * vv[3]) * f + wn * vn[3]) * inv;
+    *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) =
+        make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+  }
+  // q_t for the next pass's decisions
+  {
+    const uint4* qs = reinterpret_cast<const uint4*>(p.q + (size_t)unit * g * D);
+    uint4* qd = reinterpret_cast<uint4*>(p.q_prev + (size_t)unit * g * D);
+    for (int i = lane; i < g * D / 8; i += 32) qd[i] = __ldg(qs + i);
+  }
+  __syncwarp();  // every lane's reads of the victim's rows are done
+  // a2: the new token's K / V into the slot (pre-swizzled rows)
+  constexpr int NCH = D / 8;
+  if (lane < 2 * NCH) {
+    const bool isv = lane >= NCH;
+    const int ch = isv ? lane - NCH : lane;
+    const uint4 val = __ldg(reinterpret_cast<const uint4*>((isv ? p.v_new : p.k_new) + (size_t)unit * D) + ch);
+    *reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(isv ? vrow : krow) + ((ch ^ (row & 7)) << 3)) = val;
+  }
+  if (lane == 0) {
+    const size_t ix = (size_t)unit * C + slot;
+    p.ts[ix] = t;      // write refresh (D8)
+    p.start[ix] = t;   // the token's position
+    p.cnt[ix] = 1;
+    int32_t* trailer = reinterpret_cast<int32_t*>(pg0 + 2 * PAGE * D);
+    trailer[row] = t;
+    trailer[PAGE + row] = t;
+    const int used2 = evict ? used : used + 1;
+    p.plan[unit] = make_int4(used2 < C ? used2 : -1, 1, used2, t + 1);
+    p.counter[unit] = 0;
+    if (evict) atomicAdd(p.stats + 2, 1ull);
+    atomicAdd(p.stats + 3, 1ull);
+  }
+}
+
+#ifdef RAAS_DBG_TOKD_GLOBAL
+__device__ int g_tokd_dbg[16];
+#endif
+template <int D, int NC, int S, bool TOKD>
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
+  // TOKD: the deferred token-level instantiation (p.tokd == 1); the page kernel carries none
+  // of its code
   static_assert(D == 64 || D == 128, "head_dim");
-  using Lay = DecodeLayout<D, NC, S>;
+  using Lay = DecodeLayout<D, NC, S, TOKD>;
   constexpr int KS = Lay::KS, TILE = Lay::TILE, STAGE = Lay::STAGE;
   constexpr int ROW = 2 * D;  // bytes per token row
 
@@ -457,6 +631,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
   const uint32_t base = (raw + 1023u) & ~1023u;  // 128B-swizzle atoms need 1024B alignment
   const uint32_t ring = base + Lay::OFF_RING, qbuf = base + Lay::OFF_Q;
   const uint32_t merge = base + Lay::OFF_MERGE, scr = base + Lay::OFF_SCR;
+  const uint32_t qpb = base + Lay::OFF_QP, cand = base + Lay::OFF_CAND;
   int4* sinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_SINFO);
   int4* tinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_TINFO);
   volatile int* cq = reinterpret_cast<volatile int*>(smem_raw + (base - raw) + Lay::OFF_CQ);
@@ -499,8 +674,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       const int unit0 = blockIdx.x * fu;
       for (int pg = lane; pg < min(RAAS_PREFETCH_TILES * p.split_pages, fu * p.C); pg += 32)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                         p.kvstore + ((size_t)unit0 * p.C + pg) * 2 * PAGE * D),  // unit-major
-                     "r"(2 * PAGE * D * 2)
+                         p.kvstore + ((size_t)unit0 * p.C + pg) * p.pstr),  // unit-major
+                     "r"(p.pstr * 2)
                      : "memory");
     }
   }
@@ -536,7 +711,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
-      combine_unit<D>(p, unit, nse_u, scratch, lane);
+      if constexpr (TOKD) combine_unit_tok<D>(p, unit, nse_u, scratch, lane);
+      else        combine_unit<D>(p, unit, nse_u, scratch, lane);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -561,7 +737,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         const bool hyb = p.quest_k > 0 && nf > p.quest_k;
         const int v = q0 + lane;
         if (tok) {  // token slots: used slots are the prefix [0, z), so tile v holds z - 16v rows
-          nnatt = (nplan.z + PAGE - 1) / PAGE;
+          // (tokd: z excludes the new token, which the combine adds; an empty unit still
+          // gets one empty tile so that its combine runs)
+          nnatt = max((nplan.z + PAGE - 1) / PAGE, TOKD ? 1 : 0);
           nphys = v;
           ncnt = (lane < SP && v < nnatt) ? min(PAGE, nplan.z - PAGE * v) : 0;
         } else {
@@ -605,9 +783,16 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       const int par = k & 1;
       RAAS_TIMED(0, mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1));  // tile k-2 merged: slots free
       if (lane == 0) {
-        tinfo[2 * par] = make_int4(unit, split, (natt + SP - 1) / SP, n);
-        tinfo[2 * par + 1] = make_int4((int)j, 0, owned_cur ? 1 : 0, 0);
-        mbar_arrive_expect_tx(qfull(par), g * D * 2);
+        tinfo[3 * par] = make_int4(unit, split, (natt + SP - 1) / SP, n);
+        tinfo[3 * par + 1] = make_int4((int)j, 0, owned_cur ? 1 : 0, 0);
+        if constexpr (TOKD) {  // deferred decisions: npin, pending flag, their time stamp (t - 1)
+          tinfo[3 * par + 2] = make_int4(__ldg(p.npin + unit), pl.y, pl.w - 1, 0);
+          mbar_arrive_expect_tx(qfull(par), 2 * g * D * 2 + 32);
+          bulk_load(qpb + par * Lay::QPBUF, p.q_prev + (size_t)unit * g * D, g * D * 2, qfull(par));
+          bulk_load(qpb + par * Lay::QPBUF + Lay::QBUF, p.lse_prev + (size_t)unit * 8, 32, qfull(par));
+        } else {
+          mbar_arrive_expect_tx(qfull(par), g * D * 2);
+        }
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
         if (n < NC) mbar_arrive_cnt(mfull(par), (NC - n) * 32);  // warps with no page here
       }
@@ -626,13 +811,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           const int s = (int)(jj % S);
           RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
           // the tile the new token goes to, its row count and the row it is written to
-          const bool is_slot = tok ? page == (slot >> 4) : page == slot;
+          const bool is_slot = TOKD ? false : tok ? page == (slot >> 4) : page == slot;
           const int patch = !is_slot ? -1 : (tok ? (slot & (PAGE - 1)) : off);
           sinfo[2 * s] = make_int4(unit, page, (is_slot && !tok) ? off + 1 : c, patch);
           sinfo[2 * s + 1] =
               make_int4(k, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
-          mbar_arrive_expect_tx(full(s), STAGE);
-          bulk_load_hint(ring + s * STAGE, p.kvstore + (size_t)(unit * C + page) * 2 * PAGE * D,
+          mbar_arrive_expect_tx(full(s), STAGE);  // tokd: the trailer comes with the page
+          bulk_load_hint(ring + s * STAGE, p.kvstore + (size_t)(unit * C + page) * p.pstr,
                          STAGE, full(s), pol);
         }
         __syncwarp();
@@ -652,7 +837,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     const int par = k & 1;  // END for the merge warp
     mbar_wait(tfree(par), ((k >> 1) & 1) ^ 1);
     if (lane == 0) {
-      tinfo[2 * par + 1] = make_int4(0, FLAG_END, 0, 0);
+      tinfo[3 * par + 1] = make_int4(0, FLAG_END, 0, 0);
       mbar_arrive_cnt(mfull(par), NC * 32);
     }
     dbg_add(8, t_start);
@@ -679,7 +864,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     for (int k = 0;; ++k) {
       const int par = k & 1;
       RAAS_TIMED(2, mbar_wait(mfull(par), (k >> 1) & 1));
-      const int4 t0 = tinfo[2 * par], t1 = tinfo[2 * par + 1];
+      const int4 t0 = tinfo[3 * par], t1 = tinfo[3 * par + 1];
       if (t1.y & FLAG_END) {
         for (int e = 0; e < Lay::NPOP; ++e) push(-1);
         break;
@@ -695,10 +880,11 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         M0 = fmaxf(M0, lds_f32(dep + 128 * (KS * 4 + 0)));
         M1 = fmaxf(M1, lds_f32(dep + 128 * (KS * 4 + 1)));
       }
+      const float M0b = M0 == -INFINITY ? 0.f : M0, M1b = M1 == -INFINITY ? 0.f : M1;  // empty tile
       for (int i = 0; i < nw; ++i) {
         const uint32_t dep = merge + (par * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
-        const float s0 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 0)) - M0);
-        const float s1 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 1)) - M1);
+        const float s0 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 0)) - M0b);
+        const float s1 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 1)) - M1b);
         L0 += s0 * lds_f32(dep + 128 * (KS * 4 + 2));
         L1 += s1 * lds_f32(dep + 128 * (KS * 4 + 3));
 #pragma unroll
@@ -709,10 +895,26 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           acc[4 * mt + 3] += s1 * lds_f32(dep + 128 * (4 * mt + 3));
         }
       }
+      int4 ck = make_int4(-1, -1, -1, 0);  // tokd: the tile's victim candidate (min key)
+      if constexpr (TOKD) {
+        if (lane < nw) {
+          const uint32_t ca = cand + (par * NC + (J + lane) % NC) * 16;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(ck.x), "=r"(ck.y), "=r"(ck.z), "=r"(ck.w) : "r"(ca));
+        }
+        unsigned long long key = (static_cast<unsigned long long>(static_cast<uint32_t>(ck.y)) << 32) |
+                                 static_cast<uint32_t>(ck.x);
+        const unsigned long long kmin = warp_min_u64(key);
+        const unsigned hit = __ballot_sync(0xffffffffu, key == kmin);
+        ck.z = __shfl_sync(0xffffffffu, ck.z, __ffs(hit) - 1);
+        ck.x = static_cast<int>(static_cast<uint32_t>(kmin));
+        ck.y = static_cast<int>(static_cast<uint32_t>(kmin >> 32));
+      }
       __syncwarp();
       mbar_arrive(tfree(par));  // deposits / q / info of tile k consumed (each lane's reads)
       // publish the tile's split-K partial (m, l, acc) in the C-fragment layout
       const int pbase = (unit * p.nsplit + split) * g;
+      if (TOKD && lane == 0) p.part_key[unit * p.nsplit + split] = ck;
       if (lane < 4) {
         if (2 * qd < g) p.part_ml[pbase + 2 * qd] = make_float2(M0, L0);
         if (2 * qd + 1 < g) p.part_ml[pbase + 2 * qd + 1] = make_float2(M1, L1);
@@ -750,6 +952,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
     float acc[KS][4];
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
     uint32_t qb[KS][2];
+    // tokd: previous step's q fragments and LSE, its pending-decision info, the tile's running
+    // victim candidate, and this warp's decision counters (kept on the qd == 0 lanes)
+    uint32_t qp[KS][2];
+    float lp0 = INFINITY, lp1 = INFINITY;
+    int npin_t = 0, pend_t = 0, tm1 = 0, cslot = -1, n_dec = 0, n_stamp = 0;
+    unsigned long long ckey = ~0ull;
 #pragma unroll
     for (int mt = 0; mt < KS; ++mt) {
       acc[mt][0] = acc[mt][1] = acc[mt][2] = acc[mt][3] = 0.f;
@@ -761,6 +969,14 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
       const int4 i0 = sinfo[2 * s], i1 = sinfo[2 * s + 1];
       const int flags = i1.y;
       if (flags & FLAG_END) {
+        if constexpr (TOKD) {  // deferred decisions taken by this warp over the whole launch
+          n_dec = warp_sum_i(n_dec);
+          n_stamp = warp_sum_i(n_stamp);
+          if (lane == 0 && n_dec) {
+            atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
+            atomicAdd(p.stats + 1, (unsigned long long)n_dec);
+          }
+        }
         if constexpr (Lay::JOIN) combine_loop(ring + w * STAGE);  // join the tail's combines
         break;
       }
@@ -784,6 +1000,43 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           qb[ks][0] = r < g ? lds_u32(qrow + ks * 32) : 0u;       // d = 16ks + 2qd, +1
           qb[ks][1] = r < g ? lds_u32(qrow + ks * 32 + 16) : 0u;  // d = 16ks + 8 + 2qd, +1
         }
+        if constexpr (TOKD) {
+          const int4 ti = tinfo[3 * par + 2];
+          npin_t = ti.x;
+          pend_t = ti.y;
+          tm1 = ti.z;
+          const uint32_t qprow = qpb + par * Lay::QPBUF + r * D * 2 + qd * 4;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            qp[ks][0] = r < g ? lds_u32(qprow + ks * 32) : 0u;
+            qp[ks][1] = r < g ? lds_u32(qprow + ks * 32 + 16) : 0u;
+          }
+          const uint32_t lpa = qpb + par * Lay::QPBUF + Lay::QBUF;
+#ifdef RAAS_DBG_TOKD_GLOBAL
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            if (r < g) {
+              const uint32_t* gq = reinterpret_cast<const uint32_t*>(p.q_prev + ((size_t)unit * g + r) * D);
+              if (qp[ks][0] != __ldcg(gq + ks * 8 + qd) || qp[ks][1] != __ldcg(gq + ks * 8 + 4 + qd)) {
+                if (atomicOr(p.status, 8u) == 0u) {
+                  g_tokd_dbg[0] = unit; g_tokd_dbg[1] = page; g_tokd_dbg[2] = k; g_tokd_dbg[3] = par;
+                  g_tokd_dbg[4] = tm1; g_tokd_dbg[5] = pend_t; g_tokd_dbg[6] = (int)qp[ks][0];
+                  g_tokd_dbg[7] = (int)__ldcg(gq + ks * 8 + qd); g_tokd_dbg[8] = blockIdx.x; g_tokd_dbg[9] = w;
+                  g_tokd_dbg[10] = r; g_tokd_dbg[11] = ks; g_tokd_dbg[12] = flags;
+                }
+              }
+            }
+          }
+          lp0 = 2 * qd < g ? __ldcg(p.lse_prev + unit * 8 + 2 * qd) : INFINITY;
+          lp1 = 2 * qd + 1 < g ? __ldcg(p.lse_prev + unit * 8 + 2 * qd + 1) : INFINITY;
+          if (lp0 != (2 * qd < g ? lds_f32(lpa + 8 * qd) : INFINITY)) atomicOr(p.status, 4u);
+#else
+          lp0 = 2 * qd < g ? lds_f32(lpa + 8 * qd) : INFINITY;  // head 2qd (+inf: not a head)
+          lp1 = 2 * qd + 1 < g ? lds_f32(lpa + 8 * qd + 4) : INFINITY;
+#endif
+          ckey = ~0ull;
+          cslot = -1;
+        }
       }
 
       if (patch >= 0) {  // a2: the new token's K/V into row `patch` (smem tile + HBM store)
@@ -798,8 +1051,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(sa), "r"(val.x),
                        "r"(val.y), "r"(val.z), "r"(val.w)
                        : "memory");
-          *reinterpret_cast<uint4*>(p.kvstore + ((size_t)(unit * C + page) * 2 * PAGE +
-                                                 (isv ? PAGE : 0) + patch) * D + phys * 8) = val;
+          *reinterpret_cast<uint4*>(p.kvstore + (size_t)(unit * C + page) * p.pstr +
+                                    ((isv ? PAGE : 0) + patch) * D + phys * 8) = val;
           fence_proxy_async_smem();  // before the stage is refilled by TMA
         }
         __syncwarp();
@@ -816,6 +1069,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
 #endif
       // ---- a3/a4: S^T = K_page Q^T (M = 16 tokens, N = 8 heads, K = D) ----
       float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+      float e0[4] = {0.f, 0.f, 0.f, 0.f}, e1[4] = {0.f, 0.f, 0.f, 0.f};  // tokd: K q_prev^T
+      const bool dec = TOKD && pend_t;
       {
         const uint32_t krow = kb + (ri + 8 * (mi & 1)) * ROW;
 #pragma unroll
@@ -825,6 +1080,55 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
           ldsm_x4(krow + ((chunk ^ ri) << 4), a);
           if (ks & 1) mma_bf16_16816(c1, a, qb[ks][0], qb[ks][1]);
           else        mma_bf16_16816(c0, a, qb[ks][0], qb[ks][1]);
+          if (TOKD && dec) {
+            if (ks & 1) mma_bf16_16816(e1, a, qp[ks][0], qp[ks][1]);
+            else        mma_bf16_16816(e0, a, qp[ks][0], qp[ks][1]);
+          }
+        }
+      }
+      if constexpr (TOKD) {
+        // deferred a6 (step t-1's stamps, PAPER.md :98-100 at token level) and a7 candidates:
+        // row r and r + 8 of this tile, decision x = max_h (s'_h - LSE'_h) > log2(alpha)
+        const uint32_t tb = kb + 2 * TILE;  // the page's trailer: ts[16], start[16]
+        const int rows[2] = {r, r + 8};
+        float xr[2];
+        xr[0] = fmaxf((e0[0] + e1[0]) * p.scale_log2 - lp0, (e0[1] + e1[1]) * p.scale_log2 - lp1);
+        xr[1] = fmaxf((e0[2] + e1[2]) * p.scale_log2 - lp0, (e0[3] + e1[3]) * p.scale_log2 - lp1);
+        unsigned long long kmin = ~0ull;
+        int rmin = 0;
+#pragma unroll
+        for (int hr = 0; hr < 2; ++hr) {
+          float x = xr[hr];
+          x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1));
+          x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
+          const int row = rows[hr], e = page * PAGE + row;
+          const bool valid = row < cnt && e >= npin_t;
+          int tsv = (int)lds_u32(tb + 4 * row);
+          const int stv = (int)lds_u32(tb + 64 + 4 * row);
+          const bool stamp = dec && valid && x > p.log2_alpha;  // strict (D3)
+          if (stamp) tsv = tm1;
+          if (qd == 0) {
+            n_dec += (dec && valid) ? 1 : 0;
+            n_stamp += stamp ? 1 : 0;
+            if (stamp) {
+              p.ts[(size_t)unit * p.Ce + e] = tm1;
+              reinterpret_cast<int32_t*>(p.kvstore + (size_t)(unit * C + page) * p.pstr + 2 * PAGE * D)[row] = tm1;
+            }
+          }
+          const unsigned long long key = valid ? cand_key(tsv, stv) : ~0ull;
+          if (key < kmin) { kmin = key; rmin = row; }
+        }
+        // page minimum over the 8 row lanes (keys are unique: start positions differ)
+        unsigned long long pk = kmin;
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          const unsigned long long w2 = __shfl_xor_sync(0xffffffffu, pk, o);
+          pk = w2 < pk ? w2 : pk;
+        }
+        if (pk < ckey) {  // warp-uniform; the lane (and row) holding the page minimum
+          const unsigned hit = __ballot_sync(0xffffffffu, kmin == pk);
+          ckey = pk;
+          cslot = page * PAGE + __shfl_sync(0xffffffffu, rmin, __ffs(hit) - 1);
         }
       }
       // V^T fragments now, so the stage can be handed back to the producer before the softmax
@@ -932,13 +1236,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         sc0 = __shfl_sync(0xffffffffu, v[0], lane_of(2 * qd)) * p.scale_log2;
         sc1 = __shfl_sync(0xffffffffu, v[0], lane_of(2 * qd + 1)) * p.scale_log2;
       }
-      if (tok) {  // a4, token level (§3.2): every row's logit per head
+      if (tok) {  // a4, token level (§3.2): every row's logit per head (tokd: none, deferred)
         float* px = p.pmax + ((size_t)(unit * C + page) * PAGE + r) * g;
-        if (r < cnt) {
+        if (!TOKD && r < cnt) {
           if (2 * qd < g) px[2 * qd] = s0;
           if (2 * qd + 1 < g) px[2 * qd + 1] = s1;
         }
-        if (r + 8 < cnt) {
+        if (!TOKD && r + 8 < cnt) {
           if (2 * qd < g) px[8 * g + 2 * qd] = s2;
           if (2 * qd + 1 < g) px[8 * g + 2 * qd + 1] = s3;
         }
@@ -948,11 +1252,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         if (2 * qd + 1 < g) pmx[2 * qd + 1] = sc1;
       }
       const float mn0 = fmaxf(m0, pm0), mn1 = fmaxf(m1, pm1);
-      const float cr0 = fast_exp2(m0 - mn0), cr1 = fast_exp2(m1 - mn1);
+      // reference maxima: 0 while nothing is valid yet (an empty tile in the token mode)
+      const float mb0 = mn0 == -INFINITY ? 0.f : mn0, mb1 = mn1 == -INFINITY ? 0.f : mn1;
+      const float cr0 = fast_exp2(m0 - mb0), cr1 = fast_exp2(m1 - mb1);
       m0 = mn0;
       m1 = mn1;
-      const float p0 = fast_exp2(s0 - mn0), p1 = fast_exp2(s1 - mn1);
-      const float p2 = fast_exp2(s2 - mn0), p3 = fast_exp2(s3 - mn1);
+      const float p0 = fast_exp2(s0 - mb0), p1 = fast_exp2(s1 - mb1);
+      const float p2 = fast_exp2(s2 - mb0), p3 = fast_exp2(s3 - mb1);
       l0 = l0 * cr0 + (p0 + p2);
       l1 = l1 * cr1 + (p1 + p3);
 #pragma unroll
@@ -983,6 +1289,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S>::THREADS, 1)
         sts_f32(dep + 128 * (KS * 4 + 1), m1);
         sts_f32(dep + 128 * (KS * 4 + 2), l0);
         sts_f32(dep + 128 * (KS * 4 + 3), l1);
+        if (TOKD && lane == 0) {  // the tile's victim candidate of this warp
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(cand + (par * NC + w) * 16),
+                       "r"(static_cast<uint32_t>(ckey)), "r"(static_cast<uint32_t>(ckey >> 32)),
+                       "r"(cslot), "r"(0)
+                       : "memory");
+        }
         __syncwarp();
         mbar_arrive(mfull(par));  // each lane releases its own deposit writes
       }

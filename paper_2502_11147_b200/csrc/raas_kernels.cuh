@@ -49,6 +49,17 @@ struct DecodeParams {
   // metadata entries: Ce = L / ep per unit, ep tokens each (ep = 16: pages, the tiles C = Ce;
   // ep = 1: token-level RaaS of PAPER.md §3.2 (NEXT-3), slot s = row s % 16 of tile s / 16)
   int Ce, ep;
+  int pstr;  // bf16 elements per page in the KV store: 2 * 16 * D (+ 64: tokd trailer of the
+             // tile's 16 ts and 16 start values, copied with the page in ONE bulk copy)
+  // token level, threshold rule, per-head tables: DEFERRED stamping (NEXT-3).
+  // The step-t decisions need LSE_t, known only after the step-t pass; they are taken in the
+  // step-(t+1) pass, row by row, from the stored q_t and LSE_t (an extra S = K q_t^T on the
+  // same tile), together with the victim candidates.  The step-(t+1) pass therefore attends
+  // the L resident rows, and the combine removes the victim's row and adds the new token.
+  int tokd;
+  __nv_bfloat16* q_prev;  // [units][g][D] q of the previous step (tokd)
+  float* lse_prev;        // [units][8] its log2-domain LSE per q-head (tokd)
+  int4* part_key;         // [units][nsplit] victim candidate per split: {key lo, key hi, slot}
   int score_mode;    // 0 exact page max (D4), 1 Quest representative-key bound (D22)
   int stamp_rule;    // 0 threshold alpha (D2/D3), 1 top-r fraction of pages (D23)
   float top_r;
@@ -172,7 +183,7 @@ template <int D>
 __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
                                   const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kvstore,
                                   const int32_t* __restrict__ plen, int units, int n_kv_heads,
-                                  int P_max, int C) {
+                                  int P_max, int C, int pstr) {
   // k, v: [units][P_max][D]; unit u = (b, kv-head) copies its request's first plen[b] tokens
   constexpr int NCH = D / 8;
   const size_t total = (size_t)units * P_max * NCH;
@@ -184,7 +195,7 @@ __global__ void raas_prefill_copy(const __nv_bfloat16* __restrict__ k,
     const size_t u = src / P_max;
     if (j >= plen[u / n_kv_heads]) continue;
     const int r = j % PAGE;
-    const size_t dst = ((u * C + j / PAGE) * 2 * PAGE + r) * D + (ch ^ (r & 7)) * 8;
+    const size_t dst = (u * C + j / PAGE) * pstr + (size_t)r * D + (ch ^ (r & 7)) * 8;
     *reinterpret_cast<uint4*>(kvstore + dst) =
         __ldg(reinterpret_cast<const uint4*>(k + src * D) + ch);
     *reinterpret_cast<uint4*>(kvstore + dst + PAGE * D) =
@@ -220,7 +231,7 @@ __global__ void raas_meta_init(int32_t* ts, int32_t* start, int32_t* cnt, int32_
 // One warp per unit.  Reads t from plan[u].w - 1.
 __global__ void raas_refresh(const int32_t* ts, const int32_t* start, const int32_t* cnt,
                              const int32_t* npin, int4* plan, int32_t* counter, uint32_t* status,
-                             int units, int C, int ep) {
+                             int units, int C, int ep, int tokd) {
   const int unit = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (unit >= units) return;
@@ -248,7 +259,10 @@ __global__ void raas_refresh(const int32_t* ts, const int32_t* start, const int3
   const int victim = warp_argmin_page(best);
   if (lane == 0) {
     int4 pl;
-    if (cur_key == 0) {
+    if (tokd) {
+      // deferred token-level plan: {fill slot or -1, pending decisions, used rows, t + 1}
+      pl = make_int4(used < C ? used : -1, 0, used, t + 1);
+    } else if (cur_key == 0) {
       pl = make_int4(0, 0, 1, t + 1);  // nothing resident yet (P == 0): open page 0
     } else {
       const int cur = (int)(cur_key & 0xffffffffu) - 1;
@@ -256,6 +270,66 @@ __global__ void raas_refresh(const int32_t* ts, const int32_t* start, const int3
     }
     plan[unit] = pl;
     counter[unit] = 0;
+  }
+}
+
+// Deferred token-level stamping (tokd): apply the decisions still pending from the last step
+// (before a state readout).  One block per unit; x_j = max_h (scale q_h . k_j - LSE_h) in the
+// log2 domain from the stored q and LSE, stamp iff x_j > log2(alpha) (strict, D3), unpinned rows.
+template <int D>
+__global__ void raas_tok_flush(__nv_bfloat16* kvstore,
+                               const __nv_bfloat16* __restrict__ q_prev,
+                               const float* __restrict__ lse_prev, int32_t* ts,
+                               const int32_t* __restrict__ npin, int4* plan,
+                               unsigned long long* stats, int C, int g, float scale_log2,
+                               float log2_alpha, int pstr) {
+  const int unit = blockIdx.x;
+  const int4 pl = plan[unit];
+  if (pl.y == 0) return;  // nothing pending
+  const int used = pl.z, tm1 = pl.w - 1, np = npin[unit];
+  __shared__ float qs[MAX_GROUP][D];
+  __shared__ int cnt_s[2];
+  for (int i = threadIdx.x; i < g * D; i += blockDim.x)
+    qs[i / D][i % D] = __bfloat162float(q_prev[(size_t)unit * g * D + i]);
+  if (threadIdx.x < 2) cnt_s[threadIdx.x] = 0;
+  __syncthreads();
+  int n_dec = 0, n_stamp = 0;
+  for (int j = np + threadIdx.x; j < used; j += blockDim.x) {
+    const int tile = j / PAGE, r = j % PAGE;
+    const __nv_bfloat16* krow = kvstore + (size_t)(unit * (C / PAGE) + tile) * pstr + (size_t)r * D;
+    float x = -INFINITY;
+    for (int h = 0; h < g; ++h) {
+      float acc = 0.f;
+      for (int c = 0; c < D; ++c)  // chunk c / 8 of the row is stored at chunk (c / 8) ^ (r & 7)
+        acc += qs[h][c] * __bfloat162float(krow[(((c >> 3) ^ (r & 7)) << 3) | (c & 7)]);
+      x = fmaxf(x, acc * scale_log2 - lse_prev[unit * 8 + h]);
+    }
+    ++n_dec;
+    if (x > log2_alpha) {
+      ts[(size_t)unit * C + j] = tm1;
+      reinterpret_cast<int32_t*>(kvstore + (size_t)(unit * (C / PAGE) + tile) * pstr + 2 * PAGE * D)[r] = tm1;
+      ++n_stamp;
+    }
+  }
+  atomicAdd(&cnt_s[0], n_dec);
+  atomicAdd(&cnt_s[1], n_stamp);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(stats + 0, (unsigned long long)cnt_s[1]);
+    atomicAdd(stats + 1, (unsigned long long)cnt_s[0]);
+    plan[unit].y = 0;
+  }
+}
+
+// tokd: copy the ts / start arrays into the pages' trailers (after prefill and set_state)
+__global__ void raas_tok_trailer_sync(__nv_bfloat16* kvstore, const int32_t* __restrict__ ts,
+                                      const int32_t* __restrict__ start, size_t tiles, int pstr) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tiles * 32;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t tl = i / 32;
+    const int k = (int)(i % 32);
+    const size_t e = tl * PAGE + (k & (PAGE - 1));  // entry (token slot) of this trailer word
+    reinterpret_cast<int32_t*>(kvstore + tl * pstr + (pstr - 64))[k] = k < PAGE ? ts[e] : start[e];
   }
 }
 

@@ -45,7 +45,9 @@ def _topr_band(pstar_u, p, top_r):
     return abs(pstar_u[p] - kth) <= 1e-6 * kth
 
 
-def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None):
+def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None, history=None):
+    """history: pstar of the steps since the last comparison (index -1 = this step), for state
+    read back every few steps: a differing timestamp tau is judged by the p* of step tau."""
     keys = ("t", "ts", "start", "count", "pinned")
     same = all(np.array_equal(g[k], o[k]) for k in keys)
     if same:
@@ -56,6 +58,11 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None):
     diff = np.argwhere(g["ts"] != o["ts"])
     for u, p in diff:
         ps = pstar[u, p]
+        if history is not None:
+            tau = max(int(g["ts"][u, p]), int(o["ts"][u, p]))   # the later stamp is the disputed one
+            back = int(o["t"][u]) - tau
+            if 0 <= back < len(history):
+                ps = history[-1 - back][u, p]
         if top_r is not None:
             assert _topr_band(pstar[u], p, top_r), f"top-r decision differs at unit {u} page {p}"
             res.band_events += 1
@@ -70,8 +77,11 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None):
 
 def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_every=1,
                  layer=None, oracle=None, device="cuda", on_step=None, score_mode=0,
-                 stamp_rule=0, top_r=0.5, quest_prefill_pages=0, table_scope=0, page=16):
-    """Drive both sides through the whole stream; returns LockstepResult."""
+                 stamp_rule=0, top_r=0.5, quest_prefill_pages=0, table_scope=0, page=16,
+                 state_every=1):
+    """Drive both sides through the whole stream; returns LockstepResult.  Outputs are compared
+    every `check_every` steps, the state every `state_every` of those (a state readout applies
+    the token mode's deferred stamps, so sparse readouts exercise the deferred path)."""
     B, _, P, d = stream.k_pre.shape
     if layer is None:
         layer = RaasLayer(L, alpha, Hq, Hkv, d, B, device=device, split_pages=split_pages,
@@ -86,6 +96,7 @@ def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_eve
                                    quest_prefill_pages=quest_prefill_pages, table_scope=table_scope)
         oracle.prefill(stream.k_pre, stream.v_pre, P)
     res = LockstepResult()
+    history = []
     out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=device)
     for i in range(stream.T):
         q, k, v = (to_dev(x[i], device) for x in (stream.q, stream.k, stream.v))
@@ -98,12 +109,16 @@ def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_eve
         g_out = bf16_to_f32(from_dev(out)).astype(np.float64)
         assert np.isfinite(g_out).all()
         res.max_err = max(res.max_err, float(np.abs(g_out - o_out).max()))
-        g_state = layer.raas_get_state()
-        o_state = oracle.get_state()
         tr = oracle.get_trace()
         res.evictions += int((tr["evicted"] >= 0).sum())
-        compare_state(g_state, o_state, alpha, tr["pstar"], res, layer,
-                      top_r=top_r if stamp_rule == 1 else None)
+        history.append(tr["pstar"].copy())
+        if (i + 1) % (check_every * state_every) == 0 or i + 1 == stream.T:
+            g_state = layer.raas_get_state()
+            o_state = oracle.get_state()
+            compare_state(g_state, o_state, alpha, tr["pstar"], res, layer,
+                          top_r=top_r if stamp_rule == 1 else None,
+                          history=history if state_every > 1 else None)
+            history = []
         if on_step is not None:
             on_step(i, layer, oracle, g_out, o_out)
     assert layer.raas_get_status() == 0

@@ -90,14 +90,18 @@ def test_hybrid_mode_adds_representative_keys_only(L):
 
 
 def test_token_level_arena(L):
-    """page = 1: same KV store, metadata and score rows per token instead of per page."""
+    """page = 1: the same KV store (plus a 128-byte ts/start trailer per 16-row tile in the
+    deferred mode), metadata per token instead of per page."""
     base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
     a16 = raas.raas_arena_bytes(raas.make_config(**base))
     a1 = raas.raas_arena_bytes(raas.make_config(**base, page=1))
-    units, extra_entries = 16, 2048 - 128
-    assert a1 - a16 >= units * extra_entries * (3 * 4 + 4 * 4)   # ts/start/cnt + 4 head scores
-    assert a1 - a16 <= units * extra_entries * (3 * 4 + 4 * 4) + 64 * 1024
-    assert raas.raas_arena_bytes(raas.make_config(**dict(base, page=1, stamp_rule=1, L=512))) > 0
+    units, tiles, extra_entries = 16, 128, 2048 - 128
+    meta = units * extra_entries * 3 * 4                   # ts / start / cnt per token
+    assert meta <= a1 - a16 <= meta + units * tiles * 128 + 1024 * 1024
+    # the non-deferred token path (top-r) keeps every token's score per head
+    a1r = raas.raas_arena_bytes(raas.make_config(**dict(base, L=512, page=1, stamp_rule=1)))
+    a16r = raas.raas_arena_bytes(raas.make_config(**dict(base, L=512, stamp_rule=1)))
+    assert a1r - a16r >= units * (512 - 32) * (3 * 4 + 4 * 4)
 
 
 def test_arena_is_linear_in_L_not_N(L):

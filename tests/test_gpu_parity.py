@@ -552,20 +552,25 @@ def test_request_table_sharding_bitwise_and_set_state_validation():
 # ------------------------------------------------------------------ NEXT-3: token-level RaaS (page = 1)
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,rule,scope", [
-    (1, 4, 2, 64, 32, 256, 64, 0, 0, 0),        # toy shapes, token slots
-    (2, 32, 8, 128, 40, 300, 256, 0, 0, 0),     # Llama-3.1-8B heads
-    (2, 28, 4, 128, 37, 260, 192, 3, 0, 0),     # Qwen group, ragged prompt, 3-tile splits
-    (2, 8, 2, 128, 0, 200, 128, 2, 0, 0),       # no prompt (D21)
-    (2, 8, 2, 128, 40, 260, 256, 4, 1, 0),      # top-r over tokens (r = 0.5, :135)
-    (2, 8, 2, 128, 40, 260, 256, 0, 0, 1),      # one table per request
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,T,L,sp,rule,scope,every", [
+    (1, 4, 2, 64, 32, 256, 64, 0, 0, 0, 1),        # toy shapes, token slots
+    (1, 4, 2, 64, 32, 256, 64, 0, 0, 0, 7),        # same, deferred stamps across readouts
+    (2, 32, 8, 128, 40, 300, 256, 0, 0, 0, 1),     # Llama-3.1-8B heads
+    (2, 32, 8, 128, 40, 300, 256, 0, 0, 0, 13),
+    (2, 28, 4, 128, 37, 260, 192, 3, 0, 0, 5),     # Qwen group, ragged prompt, 3-tile splits
+    (2, 8, 2, 128, 0, 200, 128, 2, 0, 0, 1),       # no prompt (D21)
+    (2, 8, 2, 128, 0, 200, 128, 2, 0, 0, 9),
+    (2, 8, 2, 128, 40, 260, 256, 4, 1, 0, 1),      # top-r over tokens (r = 0.5, :135)
+    (2, 8, 2, 128, 40, 260, 256, 0, 0, 1, 1),      # one table per request
 ])
-def test_token_level_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, rule, scope):
+def test_token_level_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, sp, rule, scope, every):
     """page = 1 (§3.2 :98-100, Fig 5): every token is its own entry with its own
-    timestamp; GPU vs oracle, bit-exact state (per token), out within 2e-2."""
+    timestamp; GPU vs oracle, bit-exact state (per token), out within 2e-2 at every step.  With
+    the threshold rule the GPU takes step t's decisions in the step-(t+1) pass; `every` > 1
+    reads the state back only every `every` steps, so those passes carry them."""
     st = waterfall_stream(700 + B + Hq + P + rule + scope, B, Hq, Hkv, d, P, T)
     res, layer, _ = run_lockstep(oracle_mod, st, L=L, alpha=1e-3, Hq=Hq, Hkv=Hkv, split_pages=sp,
-                                 stamp_rule=rule, table_scope=scope, page=1)
+                                 stamp_rule=rule, table_scope=scope, page=1, state_every=every)
     assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
     c = layer.raas_get_counters()
     assert 0 < c["stamps"] < c["decisions"]
