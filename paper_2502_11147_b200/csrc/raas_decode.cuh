@@ -1086,10 +1086,38 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
           }
         }
       }
+      int tsr[2] = {0, 0}, str2[2] = {0, 0};  // tokd: this lane's rows' ts / start (trailer)
+      if constexpr (TOKD) {
+        const uint32_t tb = kb + 2 * TILE;
+        tsr[0] = (int)lds_u32(tb + 4 * r);
+        tsr[1] = (int)lds_u32(tb + 4 * (r + 8));
+        str2[0] = (int)lds_u32(tb + 64 + 4 * r);
+        str2[1] = (int)lds_u32(tb + 64 + 4 * (r + 8));
+      }
+      // V^T fragments now, so the stage can be handed back to the producer before the softmax
+      // and PV math: the ring slot is held ~100 cycles instead of a whole page's compute
+      uint32_t va[KS][4];
+      {
+        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * ROW;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          const int chunk = 2 * mt + (mi & 1);
+          ldsm_x4_t(vrow + ((chunk ^ ri) << 4), va[mt]);
+        }
+      }
+      auto release_stage = [&]() {
+        uint32_t dep = 0;  // consume every fragment: the ldmatrix reads have completed
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) dep ^= va[mt][0] ^ va[mt][1] ^ va[mt][2] ^ va[mt][3];
+        if constexpr (TOKD) dep ^= tsr[0] ^ tsr[1] ^ str2[0] ^ str2[1];
+        asm volatile("" ::"r"(dep));
+        __syncwarp();
+        mbar_arrive(empty(s));  // stage free for the producer
+      };
+      if (p.score_mode == 0) release_stage();
       if constexpr (TOKD) {
         // deferred a6 (step t-1's stamps, PAPER.md :98-100 at token level) and a7 candidates:
         // row r and r + 8 of this tile, decision x = max_h (s'_h - LSE'_h) > log2(alpha)
-        const uint32_t tb = kb + 2 * TILE;  // the page's trailer: ts[16], start[16]
         const int rows[2] = {r, r + 8};
         float xr[2];
         xr[0] = fmaxf((e0[0] + e1[0]) * p.scale_log2 - lp0, (e0[1] + e1[1]) * p.scale_log2 - lp1);
@@ -1103,8 +1131,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
           x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
           const int row = rows[hr], e = page * PAGE + row;
           const bool valid = row < cnt && e >= npin_t;
-          int tsv = (int)lds_u32(tb + 4 * row);
-          const int stv = (int)lds_u32(tb + 64 + 4 * row);
+          int tsv = tsr[hr];
+          const int stv = str2[hr];
           const bool stamp = dec && valid && x > p.log2_alpha;  // strict (D3)
           if (stamp) tsv = tm1;
           if (qd == 0) {
@@ -1131,26 +1159,6 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
           cslot = page * PAGE + __shfl_sync(0xffffffffu, rmin, __ffs(hit) - 1);
         }
       }
-      // V^T fragments now, so the stage can be handed back to the producer before the softmax
-      // and PV math: the ring slot is held ~100 cycles instead of a whole page's compute
-      uint32_t va[KS][4];
-      {
-        const uint32_t vrow = vb + (ri + 8 * (mi >> 1)) * ROW;
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt) {
-          const int chunk = 2 * mt + (mi & 1);
-          ldsm_x4_t(vrow + ((chunk ^ ri) << 4), va[mt]);
-        }
-      }
-      auto release_stage = [&]() {
-        uint32_t dep = 0;  // consume every fragment: the ldmatrix reads have completed
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt) dep ^= va[mt][0] ^ va[mt][1] ^ va[mt][2] ^ va[mt][3];
-        asm volatile("" ::"r"(dep));
-        __syncwarp();
-        mbar_arrive(empty(s));  // stage free for the producer
-      };
-      if (p.score_mode == 0) release_stage();
       float s0 = (c0[0] + c1[0]) * p.scale_log2, s1 = (c0[1] + c1[1]) * p.scale_log2;
       float s2 = (c0[2] + c1[2]) * p.scale_log2, s3 = (c0[3] + c1[3]) * p.scale_log2;
       if (r >= cnt) s0 = s1 = -INFINITY;
