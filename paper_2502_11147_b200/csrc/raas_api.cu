@@ -268,8 +268,8 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
     const int units = h->d.units, C = h->d.C;
     cudaLaunchConfig_t qc{};
     qc.gridDim = dim3(units);
-    qc.blockDim = dim3(128);
-    qc.dynamicSmemBytes = p.g * D * 4 + 8 * C + 1024;
+    qc.blockDim = dim3(raas::QSEL_THREADS);
+    qc.dynamicSmemBytes = p.g * D * 4 + 9 * C + 16;
     qc.stream = st;
     cudaLaunchAttribute qa[1];
     qa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -371,60 +371,71 @@ __global__ void raas_repkey_kernel(const __nv_bfloat16* __restrict__ kvstore,
 
 // Per step: Quest bound of every full prompt page (max over the group's heads of
 // sum_c max(q_c min_c, q_c max_c)) and the top-K pages by (bound desc, page asc) ->
-// vmap[u][0..K) in ascending page order.  One 128-thread block per unit: 8 lanes per page for
-// the bounds (q staged in shared memory as fp32), then warp 0 selects.  Shared memory:
-// g*D*4 (q) + 8*C (ranking keys) + 1 KiB (histogram).  PDL-chained in front of the decode
-// kernel.
+// vmap[u][0..K) in ascending page order.  One 256-thread block per unit, PDL-chained in front
+// of the decode kernel.  The representative keys are static after prefill, so the first 2 * 32
+// pages' min/max rows are loaded BEFORE griddepcontrol.wait;
+// only q waits.  8 lanes per page (D/8 channels each), 32 pages per pass.  (128-thread blocks
+// that fit beside a resident decode CTA were measured slower: 2.81 vs 2.56 ms per step.)  Selection by rank:
+// page p is selected iff fewer than K keys beat its key (keys are unique), then warp 0 writes
+// the selected pages in ascending order.  Shared memory: g*D*4 (q) + 8*C (keys) + C (flags).
+constexpr int QSEL_THREADS = 256;
 template <int D>
-__global__ void __launch_bounds__(128) raas_qselect_kernel(const __nv_bfloat16* __restrict__ q,
+__global__ void __launch_bounds__(QSEL_THREADS) raas_qselect_kernel(const __nv_bfloat16* __restrict__ q,
                                     const __nv_bfloat16* __restrict__ repkey,
                                     const int32_t* __restrict__ nfull, int32_t* vmap, int units,
                                     int C, int g, int K) {
   extern __shared__ uint8_t qs_smem[];
+  constexpr int CH = D / 8;  // channels per lane
+  constexpr int PPASS = QSEL_THREADS / 8;  // pages per pass (8 lanes per page)
+  const int u = blockIdx.x;
+  const int nf = nfull[u];   // written by prefill / set_state only
+  const int sub = threadIdx.x >> 3, cl = threadIdx.x & 7;
+  // min / max of this lane's channels {32 v + 4 cl + e} (bank-conflict-free q reads) of its
+  // first two pages, as bf16x2 words, loaded before the dependency wait
+  constexpr int NV = CH / 4;
+  uint32_t mnw[2][CH / 2], mxw[2][CH / 2];
+  auto load_page = [&](int pg, int slot) {
+    const size_t pu = (size_t)u * C + (pg < C ? pg : C - 1);  // independent of nf (no wait)
+    const __nv_bfloat16* mnp = repkey + (pu * 2 + 0) * D + 4 * cl;
+    const __nv_bfloat16* mxp = repkey + (pu * 2 + 1) * D + 4 * cl;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(mnp + 32 * v));
+      const uint2 b = __ldg(reinterpret_cast<const uint2*>(mxp + 32 * v));
+      mnw[slot][2 * v] = a.x; mnw[slot][2 * v + 1] = a.y;
+      mxw[slot][2 * v] = b.x; mxw[slot][2 * v + 1] = b.y;
+    }
+  };
+  load_page(sub, 0);
+  load_page(sub + PPASS, 1);
+  const bool active = nf > K;  // block-uniform: otherwise every prompt page is attended
   pdl_wait();  // q of this step is produced by earlier work in the stream
   pdl_launch_dependents();
-  const int u = blockIdx.x;
-  const int nf = nfull[u];
-  if (nf <= K) return;  // block-uniform
+  if (!active) return;
   float* qf = reinterpret_cast<float*>(qs_smem);
   const uint32_t keys = smem_u32(qs_smem) + g * D * 4;
-  const uint32_t hist = keys + 8 * C;
+  uint8_t* selb = qs_smem + g * D * 4 + 8 * C;
   for (int i = threadIdx.x; i < g * D; i += blockDim.x)
     qf[i] = __bfloat162float(q[(size_t)u * g * D + i]);
   __syncthreads();
-  // 8 lanes per page, each over D/8 channels; 16 pages per pass of the 128-thread block
-  constexpr int CH = D / 8;  // channels per lane
-  const int sub = threadIdx.x >> 3, cl = threadIdx.x & 7;
-  for (int p0 = 0; p0 < nf; p0 += 16) {
-    const int pg = p0 + sub;
-    const bool ok = pg < nf;
-    const size_t pu = (size_t)u * C + (ok ? pg : 0);
-    const __nv_bfloat16* mnp = repkey + (pu * 2 + 0) * D + cl * CH;
-    const __nv_bfloat16* mxp = repkey + (pu * 2 + 1) * D + cl * CH;
-    uint32_t mnw[CH / 2], mxw[CH / 2];
-#pragma unroll
-    for (int v = 0; v < CH / 8; ++v) {
-      const uint4 a = __ldg(reinterpret_cast<const uint4*>(mnp) + v);
-      const uint4 b = __ldg(reinterpret_cast<const uint4*>(mxp) + v);
-      mnw[4 * v] = a.x; mnw[4 * v + 1] = a.y; mnw[4 * v + 2] = a.z; mnw[4 * v + 3] = a.w;
-      mxw[4 * v] = b.x; mxw[4 * v + 1] = b.y; mxw[4 * v + 2] = b.z; mxw[4 * v + 3] = b.w;
-    }
+  // bound of page pg from min / max words held in registers (compile-time indexed)
+  auto do_page = [&](const uint32_t (&mn)[CH / 2], const uint32_t (&mx)[CH / 2], int pg) {
     float sc = -INFINITY;
 #pragma unroll
     for (int h = 0; h < MAX_GROUP; ++h) {
       if (h < g) {
-        const float4* qh = reinterpret_cast<const float4*>(qf + h * D + cl * CH);
+        const float4* qh = reinterpret_cast<const float4*>(qf + h * D + 4 * cl);
         float U = 0.f;
 #pragma unroll
-        for (int c4 = 0; c4 < CH / 4; ++c4) {
-          const float4 qv = qh[c4];
+        for (int c4 = 0; c4 < NV; ++c4) {
+          const float4 qv = qh[8 * c4];  // channels 32 c4 + 4 cl + (0..3)
           const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int c = 4 * c4 + e;
             const uint32_t sh = (c & 1) ? 0u : 16u;
-            const float a = __uint_as_float((mnw[c >> 1] << sh) & 0xffff0000u);
-            const float b = __uint_as_float((mxw[c >> 1] << sh) & 0xffff0000u);
+            const float a = __uint_as_float((mn[c >> 1] << sh) & 0xffff0000u);
+            const float b = __uint_as_float((mx[c >> 1] << sh) & 0xffff0000u);
             U += fmaxf(qa[e] * a, qa[e] * b);
           }
         }
@@ -434,24 +445,38 @@ __global__ void __launch_bounds__(128) raas_qselect_kernel(const __nv_bfloat16* 
         sc = fmaxf(sc, U);
       }
     }
-    if (ok && cl == 0) {
+    if (pg < nf && cl == 0) {
       const unsigned long long key = rank_key(sc, (uint32_t)pg);
       asm volatile("st.shared.u64 [%0], %1;" ::"r"(keys + 8 * pg), "l"(key) : "memory");
     }
+  };
+  do_page(mnw[0], mxw[0], sub);
+  if (nf > PPASS) do_page(mnw[1], mxw[1], sub + PPASS);
+  for (int p0 = 2 * PPASS; p0 < nf; p0 += PPASS) {  // pages beyond the prefetched ones
+    load_page(p0 + sub, 0);
+    do_page(mnw[0], mxw[0], p0 + sub);
+  }
+  __syncthreads();
+  // rank of every page's key among the nf keys; selected iff fewer than K are larger
+  for (int pg = threadIdx.x; pg < nf; pg += blockDim.x) {
+    unsigned long long kp;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(kp) : "r"(keys + 8 * pg));
+    int above = 0;
+#pragma unroll 8
+    for (int j = 0; j < nf; ++j) {
+      unsigned long long kj;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(kj) : "r"(keys + 8 * j));
+      above += kj > kp ? 1 : 0;
+    }
+    selb[pg] = above < K ? 1 : 0;
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  const unsigned long long kth = warp_kth_largest(keys, hist, nf, K, lane);
   int base = 0;
   for (int c0 = 0; c0 < nf; c0 += 32) {  // ascending compaction of the selected pages
     const int pg = c0 + lane;
-    bool sel = false;
-    if (pg < nf) {
-      unsigned long long key;
-      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(key) : "r"(keys + 8 * pg));
-      sel = key >= kth;
-    }
+    const bool sel = pg < nf && selb[pg];
     const unsigned b = __ballot_sync(0xffffffffu, sel);
     if (sel) vmap[(size_t)u * C + base + __popc(b & ((1u << lane) - 1))] = pg;
     base += __popc(b);

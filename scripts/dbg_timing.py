@@ -14,6 +14,7 @@ ap.add_argument("--P", type=int, default=256); ap.add_argument("--sp", type=int,
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--table-scope", type=int, default=0)
 ap.add_argument("--page", type=int, default=16)
+ap.add_argument("--quest", type=int, default=0, help="Quest-on-prefill hybrid: prompt pages attended")
 a = ap.parse_args()
 B, Hq, Hkv, d, P, L = a.B, a.Hq, a.Hkv, 128, a.P, a.L
 C, Pp, U = L // 16, P // 16, B * Hkv
@@ -23,18 +24,19 @@ if a.table_scope:  # one table per request: replicate kv-head 0's state
     for k in ("t", "ts", "start", "count", "pinned"):
         v = meta[k].reshape(B, Hkv, *meta[k].shape[1:])
         meta[k] = np.ascontiguousarray(np.repeat(v[:, :1], Hkv, axis=1).reshape(meta[k].shape))
-layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=a.sp, table_scope=a.table_scope, page=a.page)
+layers = [RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=a.sp, table_scope=a.table_scope, page=a.page,
+                    quest_prefill_pages=a.quest)
           for _ in range(a.layers)]
 print(layers[0].raas_launch_info())
 q = torch.randn(B, Hq, d, device="cuda").bfloat16(); kv = torch.randn(B, Hkv, d, device="cuda").bfloat16()
 out = torch.empty_like(q)
 for ly in layers:
-    if a.page == 16:
+    if a.page == 16 and not a.quest:
         ly.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"])
     else:  # token slots: prefill, then decode until every slot is used
         kp = torch.randn(B, Hkv, P, d, device="cuda").bfloat16()
         ly.raas_prefill(kp, kp, P)
-        for i in range(L - P + 8):
+        for i in range(L - P + 8 if a.page == 1 else (L - P) + 16):
             ly.raas_decode_step(q, kv, kv, out)
 L_ = raas.lib(); L_.raas_debug_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros((1024, 16), np.uint64)
