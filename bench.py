@@ -125,6 +125,26 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def variant_name(args):
+    """The non-default method options of this run, '' for the default."""
+    v = []
+    if args.score != "exact":
+        v.append(f"score={args.score}")
+    if args.top_r > 0:
+        v.append(f"top-r={args.top_r}")
+    if args.table_scope:
+        v.append("table=request")
+    if args.page != 16:
+        v.append(f"page={args.page}")
+    if args.P:
+        v.append(f"P={args.P}")
+    if args.quest_prefill:
+        v.append(f"hybrid K={args.quest_prefill}")
+    if args.split_pages:
+        v.append(f"split={args.split_pages}")
+    return ", ".join(v)
+
+
 def ncu_traffic(workload):
     """dram read+write bytes per launch of the dominant kernel, from the committed ncu
     summary (profiles/ncu_traffic.json, written from an `ncu --set full` capture)."""
@@ -413,6 +433,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
                    "quest_prefill_pages": args.quest_prefill,
                    "table_scope": "request" if args.table_scope else "kv-head",
+                   "variant": variant_name(args),
                    "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
                                    if heads else f"request-sharded x{world}, no collective"),
                    "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
