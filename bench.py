@@ -255,30 +255,53 @@ def run_ours(args, cfg, rank, world, local_rank):
                         page=args.page)
               for _ in range(nl)]
     info = layers[0].raas_launch_info()
-    for ly in layers:
-        k = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
-        v = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
-        ly.raas_prefill(k, v, P)
+    # steady state before the timed region: fill the decode pages once, then a further page cycle
+    fill_steps = (C - Pp) * 16 + 256 if args.fill < 0 else args.fill
+    fill_steps = min(fill_steps, cfg["decode"])
+    e_steps = max(4, min(args.steps, 64))
+    R = args.warmup + args.steps  # one distinct input slot (and graph) per warmup/timed step
+    if args.data == "gaussian":
+        R = 8  # i.i.d. inputs: a small ring suffices
+    qs = [torch.empty((B, hq, d), device=dev, dtype=torch.bfloat16) for _ in range(R)]
+    ks = [torch.empty((B, hkv, d), device=dev, dtype=torch.bfloat16) for _ in range(R)]
+    vs = [torch.empty((B, hkv, d), device=dev, dtype=torch.bfloat16) for _ in range(R)]
+    stream = torch.cuda.Stream(device=dev)
+    if args.data == "waterfall":
+        # PAPER.md §3.1 waterfall workload, drawn on the GPU step by step; every
+        # layer sees the same stream (distinct caches, identical contents)
+        from paper_2502_11147_b200.synth import WaterfallTorch
+
+        wf = WaterfallTorch(1000 * args.config + rank, B, hq, hkv, d, P,
+                            fill_steps + R + e_steps + 8, dev, lam=args.lam)
+        with torch.cuda.stream(stream):
+            k, v = wf.prefill()
+            for ly in layers:
+                ly.raas_prefill(k, v, P, stream=stream)
+        stream.synchronize()
         del k, v
-    R = 8  # ring of distinct per-step inputs
-    qs = [torch.randn((B, hq, d), device=dev, generator=gen).mul_(2.5).bfloat16() for _ in range(R)]
-    ks = [torch.randn((B, hkv, d), device=dev, generator=gen).bfloat16() for _ in range(R)]
-    vs = [torch.randn((B, hkv, d), device=dev, generator=gen).bfloat16() for _ in range(R)]
+        draw = lambda s_: wf.step(qs[s_], ks[s_], vs[s_])  # noqa: E731
+    else:
+        for ly in layers:
+            k = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
+            v = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
+            ly.raas_prefill(k, v, P)
+            del k, v
+        for s_ in range(R):
+            qs[s_].copy_(torch.randn((B, hq, d), device=dev, generator=gen).mul_(2.5))
+            ks[s_].copy_(torch.randn((B, hkv, d), device=dev, generator=gen))
+            vs[s_].copy_(torch.randn((B, hkv, d), device=dev, generator=gen))
+        draw = lambda s_: None  # noqa: E731
     outs = [torch.empty((B, hq, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)]
     outs_full = [torch.empty((B, hq_full, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)] if heads else None
-    stream = torch.cuda.Stream(device=dev)
 
     def eager_step(s_):  # head-sharded: decode, then the per-layer NCCL all-gather of out
         for li, ly in enumerate(layers):
             ly.raas_decode_step(qs[s_], ks[s_], vs[s_], outs[li], stream=stream)
             gather_heads(outs[li], outs_full[li])
 
-    # one CUDA graph per ring slot, each = one model step (nl decode launches)
+    # one CUDA graph per input slot, each = one model step (nl decode launches)
     graphs = []
     torch.cuda.synchronize()
-    # steady state before capture: fill the decode pages once, then a further page cycle
-    fill_steps = (C - Pp) * 16 + 256 if args.fill < 0 else args.fill
-    fill_steps = min(fill_steps, cfg["decode"])
     if not heads:
         with torch.cuda.stream(stream):
             for s in range(R):
@@ -292,21 +315,24 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_fill = time.perf_counter()
     with torch.cuda.stream(stream):  # CUDAGraph.replay() launches on the current stream
         for i in range(fill_steps):
+            draw(i % R)
             run_step(i % R)
     torch.cuda.synchronize()
     t_fill = time.perf_counter() - t_fill
-    step0 = fill_steps
     c0 = [ly.raas_get_counters() for ly in layers]
     st0 = layers[0].raas_get_state()
     Ce = L // args.page  # state entries per unit: pages, or token slots (page = 1)
     log(f"[rank {rank}] filled {fill_steps} model steps in {t_fill:.1f}s; used entries/unit="
         f"{(st0['count'] > 0).sum(1).mean():.1f}/{Ce}; launch {info}")
 
+    # the warmup and timed steps' inputs, drawn before the timed region (slot i = step i)
+    with torch.cuda.stream(stream):
+        for i in range(R if args.data == "waterfall" else 0):
+            draw(i)
     # warmup
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
-            run_step((step0 + i) % R)
-    step0 += args.warmup
+            run_step(i % R)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -318,13 +344,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for i in range(args.steps):
-                run_step((step0 + i) % R)
+                run_step((args.warmup + i) % R)
             ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
-    step0 += args.steps
     t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
@@ -369,19 +394,27 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---------------- e2e: through raas_decode_step_host with pinned host buffers -------
     e2e = None
     if not args.no_e2e and not heads:
-        hq_ = [torch.empty((B, hq, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
-        hk_ = [torch.empty((B, hkv, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
-        hv_ = [torch.empty((B, hkv, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
+        # each e2e step has its own inputs (the stream continues), staged in pinned host memory;
+        # every layer's call copies them H2D and its out D2H inside the timed region
+        ne = e_steps + 2
+        hq_ = torch.empty((ne, B, hq, d), dtype=torch.bfloat16).pin_memory()
+        hk_ = torch.empty((ne, B, hkv, d), dtype=torch.bfloat16).pin_memory()
+        hv_ = torch.empty((ne, B, hkv, d), dtype=torch.bfloat16).pin_memory()
         ho_ = [torch.empty((B, hq, d), dtype=torch.bfloat16).pin_memory() for _ in range(nl)]
-        for li in range(nl):
-            hq_[li].copy_(qs[li % R].cpu())
-            hk_[li].copy_(ks[li % R].cpu())
-            hv_[li].copy_(vs[li % R].cpu())
-        e_steps = max(4, min(args.steps, 64))
+        with torch.cuda.stream(stream):
+            for j in range(ne):
+                draw(j % R)
+                hq_[j].copy_(qs[j % R])
+                hk_[j].copy_(ks[j % R])
+                hv_[j].copy_(vs[j % R])
+        stream.synchronize()
+        e_next = [0]
 
         def e2e_step():  # one stream: H2D, step, D2H of every layer in order (no overlap)
+            j = e_next[0]
+            e_next[0] += 1
             for li, ly in enumerate(layers):
-                ly.raas_decode_step_host(hq_[li], hk_[li], hv_[li], ho_[li], stream=stream)
+                ly.raas_decode_step_host(hq_[j], hk_[j], hv_[j], ho_[li], stream=stream)
 
         for _ in range(2):
             e2e_step()
@@ -426,7 +459,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         "scaling": "strong" if heads else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)",
+        "data": (f"synthetic waterfall stream (PAPER.md §3.1 / DESIGN.md §4: sink + 2 recent pages, "
+                 f"milestones, phoenix; page-correlated keys; lambda={args.lam}), seeded torch Philox "
+                 "on the GPU, bf16, a distinct input per step" if args.data == "waterfall" else
+                 "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)"),
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
                    "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
                    "page": args.page, "alpha": args.alpha, "score_mode": args.score,
@@ -509,6 +545,10 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch")
     ap.add_argument("--layers", type=int, default=0, help="override the layer count")
     ap.add_argument("--fill", type=int, default=-1, help="decode steps before warmup (-1: auto)")
+    ap.add_argument("--data", default="waterfall", choices=["waterfall", "gaussian"],
+                    help="input stream: the waterfall workload (default) or i.i.d. Gaussian")
+    ap.add_argument("--lam", type=float, default=7.0,
+                    help="waterfall query strength (7: ~50%% page stamp rate at config 3)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

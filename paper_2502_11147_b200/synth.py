@@ -18,6 +18,8 @@ Recipes:
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 PAGE = 16
@@ -146,3 +148,91 @@ def random_steady_state(seed, units, C, Pp, t_now, page=PAGE):
         ts[u, Pp:] = ts_u[perm]
     t = np.full(units, t_now, np.int32)
     return dict(t=t, ts=ts, start=start, count=count, pinned=pinned)
+
+
+class WaterfallTorch:
+    """The ``waterfall_stream`` recipe drawn on a torch device, step by step, for the bench.
+
+    Same workload structure as ``waterfall_stream`` (sink page, the two most recent pages,
+    milestone decode pages decaying with a 256-step half-life, phoenix prefill
+    reactivations; keys share their logical page's signature), drawn with torch's Philox
+    generator so that full-size workloads (512 units x 16k steps) need no host round trip.
+    The bit patterns differ from ``waterfall_stream`` (different RNG); the oracle never
+    consumes this stream.  Inputs only: no attention, timestamps or eviction here.
+    """
+
+    def __init__(self, seed, B, Hq, Hkv, d, P, T_max, device, lam=6.0, eta=1.0, key_noise=0.5,
+                 p_milestone=0.1, milestone_half_life=256.0, p_phoenix=1.0 / 512,
+                 phoenix_len=32, recent_weight=0.8, phoenix_weight=0.8):
+        import torch
+
+        self.torch = torch
+        self.B, self.Hq, self.Hkv, self.d, self.P = B, Hq, Hkv, d, P
+        self.g = Hq // Hkv
+        self.U = B * Hkv
+        self.dev = torch.device(device)
+        self.gen = torch.Generator(device=self.dev)
+        self.gen.manual_seed(seed)
+        self.lam, self.eta, self.key_noise = lam, eta, key_noise
+        self.half_life, self.p_phoenix, self.phoenix_len = milestone_half_life, p_phoenix, phoenix_len
+        self.recent_weight, self.phoenix_weight = recent_weight, phoenix_weight
+        self.n_pages = (P + T_max + PAGE - 1) // PAGE
+        phi = torch.randn((self.U, self.n_pages, d), device=self.dev, generator=self.gen)
+        self.phi = phi / phi.norm(dim=-1, keepdim=True)
+        self.first_pos = torch.arange(self.n_pages, device=self.dev, dtype=torch.float32) * PAGE + 1
+        is_dec = self.first_pos > P
+        ms = (torch.rand((self.U, self.n_pages), device=self.dev, generator=self.gen) < p_milestone) & is_dec
+        self.ms_strength = (0.2 + 0.8 * torch.rand((self.U, self.n_pages), device=self.dev,
+                                                    generator=self.gen)) * ms
+        self.pp = (P + PAGE - 1) // PAGE
+        self.phoenix_until = torch.full((self.U,), -1, device=self.dev, dtype=torch.int64)
+        self.phoenix_page = torch.zeros((self.U,), device=self.dev, dtype=torch.int64)
+        self.i = 0                                      # decode steps drawn so far
+
+    def prefill(self, chunk=4096):
+        """Prompt K/V, bf16 [B, Hkv, P, d] (drawn in chunks of positions)."""
+        torch = self.torch
+        B, Hkv, P, d = self.B, self.Hkv, self.P, self.d
+        k = torch.empty((B, Hkv, P, d), device=self.dev, dtype=torch.bfloat16)
+        v = torch.empty_like(k)
+        kf, vf = k.view(self.U, P, d), v.view(self.U, P, d)
+        for a in range(0, P, chunk):
+            b = min(P, a + chunk)
+            pg = torch.arange(a, b, device=self.dev) // PAGE
+            z = torch.randn((self.U, b - a, d), device=self.dev, generator=self.gen)
+            kf[:, a:b] = (self.phi[:, pg] + self.key_noise * z / math.sqrt(d)).bfloat16()
+            vf[:, a:b] = torch.randn((self.U, b - a, d), device=self.dev, generator=self.gen).bfloat16()
+        return k, v
+
+    def step(self, q_out, k_out, v_out):
+        """Draw decode step i (new token at position t = P + i + 1) into bf16 tensors
+        q_out [B, Hq, d], k_out / v_out [B, Hkv, d] (on the current stream)."""
+        torch = self.torch
+        t = self.P + self.i + 1
+        cur = (t - 1) // PAGE
+        assert cur < self.n_pages, "T_max exceeded"
+        U, d = self.U, self.d
+        age = t - self.first_pos[: cur + 1]
+        decay = torch.where(age >= 0, torch.exp2(-age.clamp(min=0) / self.half_life), 0.0)
+        w = self.ms_strength[:, : cur + 1] * decay
+        w[:, 0] = torch.clamp(w[:, 0], min=1.0)                       # sink ("lazy" maps)
+        w[:, cur] = torch.clamp(w[:, cur], min=self.recent_weight)    # the two most recent pages
+        if cur >= 1:
+            w[:, cur - 1] = torch.clamp(w[:, cur - 1], min=self.recent_weight)
+        if self.pp > 0:                                               # phoenix reactivations
+            start = (torch.rand((U,), device=self.dev, generator=self.gen) < self.p_phoenix) \
+                & (self.phoenix_until < t)
+            pick = torch.randint(0, self.pp, (U,), device=self.dev, generator=self.gen)
+            self.phoenix_page = torch.where(start, pick, self.phoenix_page)
+            self.phoenix_until = torch.where(start, torch.full_like(self.phoenix_until, t + self.phoenix_len),
+                                             self.phoenix_until)
+            act = (self.phoenix_until >= t).float() * self.phoenix_weight
+            rows = torch.arange(U, device=self.dev)
+            w[rows, self.phoenix_page] = torch.maximum(w[rows, self.phoenix_page], act)
+        base = (self.lam * math.sqrt(d)) * torch.bmm(w[:, None, :], self.phi[:, : cur + 1]).squeeze(1)
+        noise = self.eta * torch.randn((U, self.g, d), device=self.dev, generator=self.gen)
+        q_out.view(U, self.g, d).copy_(base[:, None, :] + noise)
+        z = torch.randn((U, d), device=self.dev, generator=self.gen)
+        k_out.view(U, d).copy_(self.phi[:, cur] + self.key_noise * z / math.sqrt(d))
+        v_out.view(U, d).copy_(torch.randn((U, d), device=self.dev, generator=self.gen))
+        self.i += 1

@@ -720,3 +720,41 @@ def test_hybrid_with_k_at_least_prompt_pages_is_plain_raas(oracle_mod):
         assert np.array_equal(x, outs[0])
     for s_ in states[1:]:
         assert all(np.array_equal(s_[k], states[0][k]) for k in s_)
+
+
+def test_bench_waterfall_generator_is_selective(oracle_mod):
+    """The bench's device-side generator (synth.WaterfallTorch, drawn here on the CPU) keeps
+    the waterfall structure of DESIGN.md §4: keys of one logical page share a signature, and
+    the page stamp rate is selective (not the ~100 % of i.i.d. data), so eviction is not FIFO."""
+    import torch
+
+    from paper_2502_11147_b200.synth import WaterfallTorch
+
+    B, Hq, Hkv, d, P, T, L = 1, 8, 2, 64, 40, 300, 128
+    wf = WaterfallTorch(11, B, Hq, Hkv, d, P, T, "cpu", lam=7.0)
+    k, v = wf.prefill()
+    kf = k.float()[0, 0]
+    cos = torch.nn.functional.cosine_similarity(kf[:16, None], kf[None, :16], dim=-1)
+    other = torch.nn.functional.cosine_similarity(kf[:16, None], kf[None, 16:32], dim=-1)
+    assert cos.mean() > 0.6 and other.abs().mean() < 0.3          # page-correlated keys
+
+    def bits(x):
+        return x.contiguous().view(torch.int16).numpy().view(np.uint16)
+
+    o = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
+                          batch=B)
+    o.prefill(bits(k), bits(v), P)
+    q = torch.empty(B, Hq, d, dtype=torch.bfloat16)
+    kn = torch.empty(B, Hkv, d, dtype=torch.bfloat16)
+    vn = torch.empty_like(kn)
+    stamped, n_ev = [], 0
+    for i in range(T):
+        wf.step(q, kn, vn)
+        o.decode_step(bits(q), bits(kn), bits(vn), want_out=False)
+        tr, s = o.get_trace(), o.get_state()
+        m = (s["pinned"] == 0) & (s["count"] > 0)
+        stamped.extend((tr["pstar"][m] > 1e-4).tolist())
+        n_ev += int((tr["evicted"] >= 0).sum())
+    rate = float(np.mean(stamped))
+    assert n_ev > 0
+    assert 0.05 < rate < 0.95, rate
