@@ -48,8 +48,10 @@ constexpr int NC = RAAS_NC;  // consumer (MMA) warps per CTA
 constexpr int S = RAAS_S;    // K+V page stages in the ring (8 KiB each at head_dim 128)
 template <int D, bool TOKD = false>
 using Lay = raas::DecodeLayout<D, NC, S, TOKD>;
-template <int D, bool TOKD>
-constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD>; }
+// three instantiations: the default method (lean), every option at run time (gen), and the
+// deferred token level (tokd)
+template <int D, bool TOKD, bool GEN>
+constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD, GEN>; }
 
 struct Layout {
   size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, req_x, req_ctr,
@@ -61,6 +63,8 @@ struct Derived {
   int C, units, g, split_pages, nsplit;
   int Ce, ep;  // metadata entries per unit (L / page) of ep = page tokens; C = L / 16 tiles
   int tokd;    // token level with deferred stamping (page 1, threshold rule, per-head tables)
+  int gen;     // any option beyond the default method (page 16, exact score, alpha rule,
+               // per-kv-head tables, no Quest-on-prefill): the generic kernel instantiation
   int pstr;    // bf16 elements per KV page: 2 * 16 * D, + 64 (ts/start trailer) when tokd
 };
 
@@ -84,6 +88,8 @@ int derive(const raas_config* c, Derived* d) {
   d->Ce = c->L / c->page;
   d->tokd = c->page == 1 && c->stamp_rule == 0 && c->table_scope == 0 && c->score_mode == 0;
   d->pstr = 2 * raas::PAGE * c->head_dim + (d->tokd ? 64 : 0);
+  d->gen = !d->tokd && (c->page != raas::PAGE || c->score_mode != 0 || c->stamp_rule != 0 ||
+                        c->table_scope != 0 || c->quest_prefill_pages > 0);
   if (c->page == 1 && c->score_mode != 0)
     return fail(RAAS_E_UNSUPPORTED, "page = 1: the representative-key bound of one key is the key itself; use score_mode 0");
   if (c->page == 1 && c->quest_prefill_pages > 0)
@@ -290,8 +296,9 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  if (h->d.tokd) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true>(), p));
-  else           RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false>(), p));
+  if (h->d.tokd)     RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true, false>(), p));
+  else if (h->d.gen) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, true>(), p));
+  else               RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, false>(), p));
   return RAAS_OK;
 }
 
@@ -320,9 +327,9 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
   return best;
 }
 
-template <int D, bool TOKD>
+template <int D, bool TOKD, bool GEN>
 int setup_kernel_t(raas_handle* h) {
-  auto k = decode_kernel<D, TOKD>();
+  auto k = decode_kernel<D, TOKD, GEN>();
   h->smem = Lay<D, TOKD>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
@@ -333,7 +340,8 @@ int setup_kernel_t(raas_handle* h) {
 }
 template <int D>
 int setup_kernel(raas_handle* h) {
-  return h->d.tokd ? setup_kernel_t<D, true>(h) : setup_kernel_t<D, false>(h);
+  return h->d.tokd ? setup_kernel_t<D, true, false>(h)
+                   : h->d.gen ? setup_kernel_t<D, false, true>(h) : setup_kernel_t<D, false, false>(h);
 }
 
 int build_repkeys(raas_handle* h, cudaStream_t st) {

@@ -185,9 +185,13 @@ struct DecodeLayout {
 // ---------------------------------------------------------------------------------------------
 // a5-a7 for one unit, by one warp, after all its splits have published their partials.
 // ---------------------------------------------------------------------------------------------
-template <int D>
+template <int D, bool GEN>
 __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, int nse, uint32_t scr,
                                              int lane) {
+  // GEN = false: the default method (page = 16, alpha rule, one table per kv-head) with the
+  // optional rules compiled out; GEN = true: every option decided at run time
+  const bool tscope = GEN && p.table_scope != 0;
+  const bool topr = GEN && p.stamp_rule == 1;
   // Latency-oriented: the plan, the split statistics, the first block of split partials and
   // the first 128 pages' metadata are all requested before any of them is used (nse comes with
   // the queue entry), so a unit costs ~one dependent L2 round trip before its stores.
@@ -293,7 +297,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       if (h < g) x = fmaxf(x, pmv[i][h] - lse[h]);
     return x;
   };
-  if (p.table_scope != 0) {
+  if (tscope) {
     // table_scope 1 (D25): fold this kv-head's page scores into the request-wide maximum
     // early, so the reductions drain while the output is combined
     for (int pc = 0; pc < used_eff; pc += 32 * PPL) {
@@ -357,20 +361,20 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     }
   }
   // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
-  if (p.table_scope != 0 && !rq) return;  // another kv-head of the request decides
+  if (tscope && !rq) return;  // another kv-head of the request decides
   if (rq) {
 #pragma unroll
     for (int h = 0; h < MAX_GROUP; ++h) lse[h] = 0.f;  // req_x already holds normalised scores
   }
-  const int nrep = p.table_scope != 0 ? p.n_kv : 1;   // metadata replicas this warp writes
-  const int unit0 = p.table_scope != 0 ? req * p.n_kv : unit;
+  const int nrep = tscope ? p.n_kv : 1;   // metadata replicas this warp writes
+  const int unit0 = tscope ? req * p.n_kv : unit;
   auto page_key = [&](float x, int st) {  // larger key = ranked first; valid keys are > 0
     const uint32_t b = __float_as_uint(x);
     const uint32_t sx = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
     return (static_cast<unsigned long long>(sx) << 32) | (0xffffffffu - static_cast<uint32_t>(st));
   };
   unsigned long long kth = 0;
-  if (p.stamp_rule == 1) {
+  if (topr) {
     // pass 1: keys of the decision pages -> scratch (the split weights are no longer needed)
     const uint32_t scr_key = scr, scr_hist = scr + 8 * 512;
     int nd = 0;
@@ -420,7 +424,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
         }
         if (pg >= npin) {
           const float x = page_x(i);
-          const bool stamp = p.stamp_rule == 1 ? page_key(x, st_p) >= kth
+          const bool stamp = topr ? page_key(x, st_p) >= kth
                                                : x > p.log2_alpha;  // strict (D3)
           ++n_dec;
           n_stamp += stamp ? 1 : 0;
@@ -438,7 +442,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
   if (lane == 0) {
-    const int4 np = next_plan(slot, off + 1, used_eff, C, t, victim, p.status, p.ep);
+    const int4 np = next_plan(slot, off + 1, used_eff, C, t, victim, p.status, GEN ? p.ep : PAGE);
     for (int r = 0; r < nrep; ++r) p.plan[unit0 + r] = np;
     atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
     atomicAdd(p.stats + 1, (unsigned long long)n_dec);
@@ -616,9 +620,13 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 #ifdef RAAS_DBG_TOKD_GLOBAL
 __device__ int g_tokd_dbg[16];
 #endif
-template <int D, int NC, int S, bool TOKD>
+template <int D, int NC, int S, bool TOKD, bool GEN>
 __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
+  // GEN = false (and !TOKD): the default method only (page = 16, exact page score, alpha rule,
+  // per-kv-head tables, no Quest-on-prefill); the options' run-time branches are compiled out
+  const int quest_k = GEN ? p.quest_k : 0;
+  const int score_mode = GEN ? p.score_mode : 0;
   // TOKD: the deferred token-level instantiation (p.tokd == 1); the page kernel carries none
   // of its code
   static_assert(D == 64 || D == 128, "head_dim");
@@ -665,7 +673,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0 && p.quest_k == 0) {
+  if (warp == 0 && quest_k == 0) {
     // Warm L2 with this CTA's first owned tile while the previous kernel drains (its tail
     // leaves HBM idle).  Only a hint: nothing is read from these lines before griddepcontrol.wait
     // below, and L2 is the point of coherence, so a row the previous kernel rewrites is seen.
@@ -688,7 +696,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
 
   const int C = p.C, SP = p.split_pages, g = p.g;  // C: 16-row tiles (pages) per unit
   const int n_tiles = p.units * p.nsplit;
-  const bool tok = p.ep == 1;  // token-level RaaS (NEXT-3): metadata per row, tiles physical only
+  const bool tok = (GEN || TOKD) && p.ep == 1;  // token-level RaaS (NEXT-3): metadata per row, tiles physical only
 
   // multi-consumer combine queue: the combine warp from the start, the consumers after END
   auto combine_loop = [&](uint32_t scratch) {
@@ -712,7 +720,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
       if constexpr (TOKD) combine_unit_tok<D>(p, unit, nse_u, scratch, lane);
-      else        combine_unit<D>(p, unit, nse_u, scratch, lane);
+      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -733,8 +741,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       if (tl < n_tiles) {
         const int u = tl / p.nsplit, q0 = (tl - u * p.nsplit) * SP;
         nplan = p.plan[u];
-        const int nf = p.quest_k > 0 ? p.nfull[u] : 0;
-        const bool hyb = p.quest_k > 0 && nf > p.quest_k;
+        const int nf = quest_k > 0 ? p.nfull[u] : 0;
+        const bool hyb = quest_k > 0 && nf > quest_k;
         const int v = q0 + lane;
         if (tok) {  // token slots: used slots are the prefix [0, z), so tile v holds z - 16v rows
           // (tokd: z excludes the new token, which the combine adds; an empty unit still
@@ -743,8 +751,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
           nphys = v;
           ncnt = (lane < SP && v < nnatt) ? min(PAGE, nplan.z - PAGE * v) : 0;
         } else {
-          nnatt = hyb ? p.quest_k + nplan.z - nf : nplan.z;
-          nphys = !hyb ? v : (v < p.quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - p.quest_k));
+          nnatt = hyb ? quest_k + nplan.z - nf : nplan.z;
+          nphys = !hyb ? v : (v < quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - quest_k));
           ncnt = (lane < SP && v < nnatt) ? p.cnt[(size_t)u * C + nphys] : 0;
         }
       }
@@ -1114,7 +1122,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
         __syncwarp();
         mbar_arrive(empty(s));  // stage free for the producer
       };
-      if (p.score_mode == 0) release_stage();
+      if (score_mode == 0) release_stage();
       if constexpr (TOKD) {
         // deferred a6 (step t-1's stamps, PAPER.md :98-100 at token level) and a7 candidates:
         // row r and r + 8 of this tile, decision x = max_h (s'_h - LSE'_h) > log2(alpha)
@@ -1170,7 +1178,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
         pm1 = fmaxf(pm1, __shfl_xor_sync(0xffffffffu, pm1, o));
       }
       float sc0 = pm0, sc1 = pm1;  // the page score the stamp will use (log2 domain)
-      if (p.score_mode == 1) {
+      if (score_mode == 1) {
         // Quest's representative-key bound (PAPER.md :147-151, :362; reading D22): per channel
         // c, max(q_c min_c, q_c max_c) over the page's valid keys, summed over c.  Lane l owns
         // channels [l*CQ, (l+1)*CQ); the page is already in shared memory (no extra HBM bytes).
