@@ -438,7 +438,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                "unit": "decode steps/s", "steps": e_steps,
                "h2d_bytes_per_step": nl * (B * hq * d + 2 * B * hkv * d) * 2,
                "d2h_bytes_per_step": nl * B * hq * d * 2,
-               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out), one stream, layers in order"}
+               "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out: zero-copy ingest kernel + out stored to host by the combine), one stream, layers in order"}
 
     if rank != 0:
         return None

@@ -142,9 +142,13 @@ RAAS_API int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, c
 RAAS_API int raas_decode_step(raas_handle* h, const void* q, const void* k_new, const void* v_new,
                      void* out, void* stream);
 
-/* Same step with HOST buffers (same layouts): async H2D copies of q/k_new/v_new into the
- * arena's staging area, the step, async D2H copy of out.  Use pinned host memory for real
- * asynchrony; the host buffers must stay valid until the stream completes. */
+/* Same step with HOST buffers (same layouts).  Pinned (page-locked, mapped: cudaHostAlloc,
+ * torch pin_memory) inputs are read over PCIe by a small ingest kernel that runs ahead of the
+ * step (the host reads overlap the previous kernel of the stream), and a pinned `out_host` is
+ * written directly by the step's combine (zero-copy); pageable buffers go through async
+ * staging copies in the arena.  Either way the result is bitwise that of raas_decode_step.
+ * Host buffers must hold the step's data when the call is made (pinned inputs may be read
+ * before earlier work in the stream completes) and stay valid until the stream completes. */
 RAAS_API int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_host,
                           const void* v_new_host, void* out_host, void* stream);
 

@@ -538,6 +538,21 @@ int raas_decode_step(raas_handle* h, const void* q, const void* k_new, const voi
                                 : launch_decode<64>(h, q, k_new, v_new, out, st);
 }
 
+namespace {
+// Device alias of a pinned, mapped host buffer (UVA: cudaHostAlloc / torch pin_memory), or
+// nullptr for pageable memory or a misaligned pointer.
+void* mapped_alias(const void* hp, uintptr_t align) {
+  if (reinterpret_cast<uintptr_t>(hp) % align != 0) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, hp) != cudaSuccess) {
+    cudaGetLastError();  // pageable memory on older drivers: clear the sticky-free error
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
+  return at.devicePointer;
+}
+}  // namespace
+
 int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_host,
                           const void* v_new_host, void* out_host, void* stream) {
   if (!h) return fail(RAAS_E_INVALID, "null handle");
@@ -548,14 +563,40 @@ int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* a = h->arena;
   const size_t D = h->cfg.head_dim, U = h->d.units, g = h->d.g;
-  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sq, q_host, U * g * D * 2, cudaMemcpyHostToDevice, st));
-  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sk, k_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
-  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sv, v_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
+  const void* qm = mapped_alias(q_host, 16);
+  const void* km = mapped_alias(k_new_host, 16);
+  const void* vm = mapped_alias(v_new_host, 16);
+  void* om = mapped_alias(out_host, 8);
+  if (qm && km && vm) {
+    // pinned inputs: one zero-copy ingest kernel (PCIe reads overlap the previous kernel)
+    const int nq = (int)(U * g * D * 2 / 16), nkv = (int)(U * D * 2 / 16);
+    const int per_block = raas::INGEST_THREADS * raas::INGEST_PER;
+    const int blocks = std::max(1, std::min(h->num_sms, (nq + 2 * nkv + per_block - 1) / per_block));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(blocks);
+    lc.blockDim = dim3(raas::INGEST_THREADS);
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    RAAS_CUDA(cudaLaunchKernelEx(&lc, raas::raas_ingest_kernel, static_cast<const uint4*>(qm),
+                                 static_cast<const uint4*>(km), static_cast<const uint4*>(vm),
+                                 reinterpret_cast<uint4*>(a + h->lay.sq), reinterpret_cast<uint4*>(a + h->lay.sk),
+                                 reinterpret_cast<uint4*>(a + h->lay.sv), nq, nkv));
+  } else {  // pageable inputs: staged copies
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sq, q_host, U * g * D * 2, cudaMemcpyHostToDevice, st));
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sk, k_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
+    RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sv, v_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
+  }
+  // pinned out: the combine stores the bf16 rows straight into host memory
+  void* out = om ? om : a + h->lay.so;
   int rc = h->cfg.head_dim == 128
-               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, a + h->lay.so, st)
-               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, a + h->lay.so, st);
+               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st)
+               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st);
   if (rc) return rc;
-  RAAS_CUDA(cudaMemcpyAsync(out_host, a + h->lay.so, U * g * D * 2, cudaMemcpyDeviceToHost, st));
+  if (!om) RAAS_CUDA(cudaMemcpyAsync(out_host, a + h->lay.so, U * g * D * 2, cudaMemcpyDeviceToHost, st));
   return RAAS_OK;
 }
 

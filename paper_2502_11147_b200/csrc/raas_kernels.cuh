@@ -483,4 +483,53 @@ __global__ void __launch_bounds__(QSEL_THREADS) raas_qselect_kernel(const __nv_b
   }
 }
 
+// raas_decode_step_host with pinned (mapped) host buffers: one step's q / k_new / v_new are
+// read from host memory over PCIe by the SMs (zero-copy) and stored into the arena's staging
+// area.  The host reads are issued BEFORE griddepcontrol.wait (the host buffers are complete
+// when the call is made), so they overlap the previous kernel of the stream; the stores wait
+// for it (the staging area may still be read by this handle's previous step).  128-thread
+// blocks with a small register budget fit beside a resident decode CTA.  Counts in 16 B
+// vectors; element i of the concatenation [q | k | v].
+constexpr int INGEST_THREADS = 128, INGEST_PER = 4;
+__global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
+    const uint4* __restrict__ q_h, const uint4* __restrict__ k_h, const uint4* __restrict__ v_h,
+    uint4* __restrict__ q_d, uint4* __restrict__ k_d, uint4* __restrict__ v_d, int nq, int nkv) {
+  const int total = nq + 2 * nkv;
+  const int nth = gridDim.x * INGEST_THREADS;
+  const int tid = blockIdx.x * INGEST_THREADS + threadIdx.x;
+  auto ld = [&](int i) {
+    return i < nq ? ld_sys_v4(q_h + i) : i < nq + nkv ? ld_sys_v4(k_h + (i - nq)) : ld_sys_v4(v_h + (i - nq - nkv));
+  };
+  auto st = [&](int i, uint4 x) {
+    if (i < nq) q_d[i] = x;
+    else if (i < nq + nkv) k_d[i - nq] = x;
+    else v_d[i - nq - nkv] = x;
+  };
+  uint4 r[INGEST_PER];
+#pragma unroll
+  for (int j = 0; j < INGEST_PER; ++j) {
+    const int i = tid + j * nth;
+    if (i < total) r[j] = ld(i);
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+#pragma unroll
+  for (int j = 0; j < INGEST_PER; ++j) {
+    const int i = tid + j * nth;
+    if (i < total) st(i, r[j]);
+  }
+  for (int i0 = tid + INGEST_PER * nth; i0 < total; i0 += INGEST_PER * nth) {  // large batches
+#pragma unroll
+    for (int j = 0; j < INGEST_PER; ++j) {
+      const int i = i0 + j * nth;
+      if (i < total) r[j] = ld(i);
+    }
+#pragma unroll
+    for (int j = 0; j < INGEST_PER; ++j) {
+      const int i = i0 + j * nth;
+      if (i < total) st(i, r[j]);
+    }
+  }
+}
+
 }  // namespace raas

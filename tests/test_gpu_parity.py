@@ -161,22 +161,45 @@ def test_bitwise_determinism_and_request_sharding():
         assert np.array_equal(np.concatenate([slo[k], shi[k]]), sa[k])
 
 
-def test_host_entry_point_matches_device_entry_point():
+@pytest.mark.parametrize("mode", ["pinned_reused", "pinned_queued", "pageable"])
+def test_host_entry_point_matches_device_entry_point(mode):
+    """raas_decode_step_host: pinned buffers take the zero-copy path (ingest kernel + out
+    stored straight to host memory), pageable ones the staged copies; both are bitwise the
+    device entry point.  'reused' rewrites one pinned buffer every step (no stale reads);
+    'queued' enqueues every step before one synchronisation (stream order kept)."""
     B, Hq, Hkv, d, P, T, L = 2, 8, 2, 128, 40, 40, 64
     st = waterfall_stream(4, B, Hq, Hkv, d, P, T)
-    dev, _ = _run_gpu(st, L, Hq, Hkv)
+    dev, s_dev = _run_gpu(st, L, Hq, Hkv)
     layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
     layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
-    out_h = torch.empty((B, Hq, d), dtype=torch.bfloat16).pin_memory()
-    outs = []
-    for i in range(T):
-        qh = torch.from_numpy(st.q[i].view(np.int16)).view(torch.bfloat16).pin_memory()
-        kh = torch.from_numpy(st.k[i].view(np.int16)).view(torch.bfloat16).pin_memory()
-        vh = torch.from_numpy(st.v[i].view(np.int16)).view(torch.bfloat16).pin_memory()
-        layer.raas_decode_step_host(qh, kh, vh, out_h)
+
+    def host(x, pin):
+        t = torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16)
+        return t.pin_memory() if pin else t.clone()
+
+    if mode == "pinned_queued":
+        ins = [(host(st.q[i], True), host(st.k[i], True), host(st.v[i], True)) for i in range(T)]
+        outs_h = [torch.empty((B, Hq, d), dtype=torch.bfloat16).pin_memory() for _ in range(T)]
+        for i in range(T):
+            layer.raas_decode_step_host(*ins[i], outs_h[i])
         torch.cuda.current_stream().synchronize()
-        outs.append(out_h.view(torch.int16).numpy().view(np.uint16).copy())
+        outs = [o.view(torch.int16).numpy().view(np.uint16).copy() for o in outs_h]
+    else:
+        pin = mode == "pinned_reused"
+        qh, kh, vh = host(st.q[0], pin), host(st.k[0], pin), host(st.v[0], pin)
+        out_h = torch.empty((B, Hq, d), dtype=torch.bfloat16)
+        out_h = out_h.pin_memory() if pin else out_h
+        outs = []
+        for i in range(T):
+            qh.copy_(host(st.q[i], False))
+            kh.copy_(host(st.k[i], False))
+            vh.copy_(host(st.v[i], False))
+            layer.raas_decode_step_host(qh, kh, vh, out_h)
+            torch.cuda.current_stream().synchronize()
+            outs.append(out_h.view(torch.int16).numpy().view(np.uint16).copy())
     assert np.array_equal(np.stack(outs), dev)
+    s_h = layer.raas_get_state()
+    assert all(np.array_equal(s_h[k], s_dev[k]) for k in s_dev)
 
 
 def test_cuda_graph_capture_matches_eager():
