@@ -350,7 +350,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
-    t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
+    red_dev = dev if not world > 1 or torch.distributed.get_backend() == "nccl" else "cpu"
+    t_max = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     if world > 1:
         torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t_max.item())
@@ -431,7 +432,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         stream.synchronize()
         wall = time.perf_counter() - w0
         e_ms = max(e0.elapsed_time(e1), wall * 1e3)
-        te = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        te = torch.tensor([e_ms], device=red_dev, dtype=torch.float64)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": e_steps / (float(te.item()) / 1e3) * world,
@@ -590,15 +591,25 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # RAAS_BENCH_SHARE_GPU=1: test mode for the multi-rank path on a single GPU (ranks share
+    # device 0, gloo carries the barriers and the timing reduction); never a bench number
+    share = os.environ.get("RAAS_BENCH_SHARE_GPU") == "1"
     if args.impl == "reference":
         out = run_reference(args, cfg, rank, world)
     else:
         import torch
 
+        if share:
+            local_rank = local_rank % torch.cuda.device_count()
         if world > 1:
             torch.cuda.set_device(local_rank)
-            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if share:
+                torch.distributed.init_process_group("gloo")
+            else:
+                torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         out = run_ours(args, cfg, rank, world, local_rank)
+        if share and out is not None:
+            out["note"] = "RAAS_BENCH_SHARE_GPU test mode: ranks shared one GPU; not a measurement"
         if world > 1:
             torch.distributed.barrier()
             torch.distributed.destroy_process_group()
