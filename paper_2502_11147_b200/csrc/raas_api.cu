@@ -6,7 +6,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/raas.h"
@@ -206,6 +209,10 @@ void unpack_store(const uint16_t* dev, uint16_t* k, uint16_t* v, size_t pages, i
 
 }  // namespace
 
+#ifdef RAAS_DBG_TIMING
+static int g_dbg_launch = 0;  // timeline slot of the next decode launch (debug builds)
+#endif
+
 struct raas_handle {
   raas_config cfg;
   Derived d;
@@ -221,9 +228,25 @@ struct raas_handle {
 
 namespace {
 
+// Last decode handle launched on each stream (early start, DecodeParams::early).  A decode
+// kernel may read its handle's state before griddepcontrol.wait only if the kernel right before
+// it in the stream is not this handle's previous step: every kernel of the PDL chain triggers
+// its dependents after its own griddepcontrol.wait, so the kernel two back has completed.
+// Kernels launched without PDL serialise fully, which is also safe.
+std::mutex g_last_mu;
+std::unordered_map<cudaStream_t, const raas_handle*> g_last_decode;
+
+bool note_launch(const raas_handle* h, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_last_mu);
+  auto it = g_last_decode.find(st);
+  const bool same = it != g_last_decode.end() && it->second == h;
+  g_last_decode[st] = h;
+  return !same;
+}
+
 template <int D>
 int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* v_new,
-                  void* out, cudaStream_t st) {
+                  void* out, cudaStream_t st, bool after_ingest = false) {
   DecodeParams p{};
   uint8_t* a = h->arena;
   p.q = static_cast<const __nv_bfloat16*>(q);
@@ -262,6 +285,15 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   p.nfull = reinterpret_cast<const int32_t*>(a + h->lay.nfull);
   p.vmap = h->cfg.quest_prefill_pages > 0 ? reinterpret_cast<const int32_t*>(a + h->lay.vmap) : nullptr;
   p.table_scope = h->cfg.table_scope;
+#ifdef RAAS_DBG_TIMING
+  p.dbg_slot = g_dbg_launch++ & 7;
+#endif
+  {
+    const bool other = note_launch(h, st);  // always record the launch
+    // the host path's ingest kernel waited for the previous kernel before triggering us
+    static const bool no_early = std::getenv("RAAS_NO_EARLY") != nullptr;  // A/B experiments
+    p.early = (other || after_ingest) && !h->d.tokd && !h->d.gen && !no_early;
+  }
   p.n_kv = h->cfg.n_kv_heads;
   p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;
   p.req_ctr = h->cfg.table_scope ? reinterpret_cast<int32_t*>(a + h->lay.req_ctr) : nullptr;
@@ -336,6 +368,10 @@ int setup_kernel_t(raas_handle* h) {
   RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
   h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
+  if (const char* e = std::getenv("RAAS_GRID")) {  // tuning experiments only (scripts/)
+    const int G = std::atoi(e);
+    if (G > 0) h->grid = std::min(G, h->num_sms * per_sm);
+  }
   return RAAS_OK;
 }
 template <int D>
@@ -463,6 +499,11 @@ int raas_create(const raas_config* cfg, void* arena, size_t arena_bytes, int dev
 }
 
 int raas_destroy(raas_handle* h) {
+  {
+    std::lock_guard<std::mutex> lk(g_last_mu);
+    for (auto it = g_last_decode.begin(); it != g_last_decode.end();)
+      it = it->second == h ? g_last_decode.erase(it) : std::next(it);
+  }
   delete h;
   return RAAS_OK;
 }
@@ -593,8 +634,8 @@ int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_
   // pinned out: the combine stores the bf16 rows straight into host memory
   void* out = om ? om : a + h->lay.so;
   int rc = h->cfg.head_dim == 128
-               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st)
-               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st);
+               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st, true)
+               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st, true);
   if (rc) return rc;
   if (!om) RAAS_CUDA(cudaMemcpyAsync(out_host, a + h->lay.so, U * g * D * 2, cudaMemcpyDeviceToHost, st));
   return RAAS_OK;
@@ -748,6 +789,13 @@ int raas_launch_info(const raas_handle* h, int32_t info[5]) {
 // tuning experiment only (not part of the ABI in include/raas.h): read + clear the cycle counters
 RAAS_API int raas_debug_units(uint64_t* out, int n) {
   RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg_unit, sizeof(uint64_t) * n));
+  return RAAS_OK;
+}
+RAAS_API int raas_debug_timeline(uint64_t* out, int n) {  // [8][256][4], then cleared
+  RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_tl, sizeof(uint64_t) * n));
+  std::vector<uint64_t> z(8 * 256 * 4, 0);
+  RAAS_CUDA(cudaMemcpyToSymbol(raas::g_raas_tl, z.data(), z.size() * 8));
+  g_dbg_launch = 0;
   return RAAS_OK;
 }
 RAAS_API int raas_debug_timing(uint64_t* out, int n) {

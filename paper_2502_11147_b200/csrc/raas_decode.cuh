@@ -34,6 +34,8 @@ namespace raas {
 #ifdef RAAS_DBG_TIMING  // tuning experiment: per-CTA cycle accounting of the pipeline waits
 __device__ unsigned long long g_raas_dbg[1024][16];
 __device__ unsigned long long g_raas_dbg_unit[4096][4];  // cta, pushed, combine start, end
+// multi-launch timeline: [launch slot][cta] = {entry, after griddepcontrol.wait, producer end, exit}
+__device__ unsigned long long g_raas_tl[8][256][4];
 __device__ __forceinline__ long long dbg_clock() { return clock64(); }
 __device__ __forceinline__ void dbg_add(int slot, long long t0) {
   if ((threadIdx.x & 31) == 0) atomicAdd(&g_raas_dbg[blockIdx.x][slot], (unsigned long long)(clock64() - t0));
@@ -655,6 +657,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
   auto cqempty = [&](int q) { return bar + 8 * (2 * S + 6 + CQ + q); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef RAAS_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_raas_tl[p.dbg_slot & 7][blockIdx.x][0] = dbg_gtimer();
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full(s), 1);
@@ -687,11 +692,20 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
                      : "memory");
     }
   }
-  pdl_wait();  // everything above overlapped the previous kernel; state reads start here
-  pdl_launch_dependents();
+  // Early start (default method, p.early: the host saw that the previous kernel of the stream
+  // is not this handle's decode step): this handle's state was written by a kernel that
+  // completed before the previous one could trigger us, so the producer reads its first tile's
+  // metadata and issues that tile's first page copies BEFORE griddepcontrol.wait (below); only
+  // the step's inputs (q, k_new, v_new) and every store wait for the previous kernel.
+  const bool early = !GEN && !TOKD && p.early != 0;
+  if (!(early && warp == 0)) {
+    pdl_wait();  // everything above overlapped the previous kernel; state reads start here
+    pdl_launch_dependents();
+  }
   const long long t_start = dbg_clock();
 #ifdef RAAS_DBG_TIMING
   if (threadIdx.x == 0) g_raas_dbg[blockIdx.x][12] = dbg_gtimer();
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_raas_tl[p.dbg_slot & 7][blockIdx.x][1] = dbg_gtimer();
 #endif
 
   const int C = p.C, SP = p.split_pages, g = p.g;  // C: 16-row tiles (pages) per unit
@@ -740,7 +754,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     auto fetch = [&](int tl) {
       if (tl < n_tiles) {
         const int u = tl / p.nsplit, q0 = (tl - u * p.nsplit) * SP;
-        nplan = p.plan[u];
+        nplan = __ldcg(p.plan + u);
         const int nf = quest_k > 0 ? p.nfull[u] : 0;
         const bool hyb = quest_k > 0 && nf > quest_k;
         const int v = q0 + lane;
@@ -753,9 +767,36 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
         } else {
           nnatt = hyb ? quest_k + nplan.z - nf : nplan.z;
           nphys = !hyb ? v : (v < quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - quest_k));
-          ncnt = (lane < SP && v < nnatt) ? p.cnt[(size_t)u * C + nphys] : 0;
+          ncnt = (lane < SP && v < nnatt) ? __ldcg(p.cnt + (size_t)u * C + nphys) : 0;
         }
       }
+    };
+    // pages in batches, one lane per page: each lane waits for its stage, fills the stage
+    // info and issues one 1-D bulk copy of the page (K rows then V rows, 16*D*4 contiguous
+    // bytes, stored pre-swizzled in HBM so they land bank-conflict-free for ldmatrix).  A batch
+    // never spans more than S positions: a parity wait must be at most one phase ahead of its
+    // barrier.
+    constexpr int BATCH = S < 32 ? S : 32;
+    auto issue_batch = [&](int i0, int nb, uint32_t jb, int unit, int n, int kt, int cntv, int physv,
+                           int slot, int off) {
+      const int c = __shfl_sync(0xffffffffu, cntv, (i0 + lane) & 31);
+      const int page = __shfl_sync(0xffffffffu, physv, (i0 + lane) & 31);
+      if (lane < nb) {
+        const int i = i0 + lane;
+        const uint32_t jj = jb + lane;
+        const int s = (int)(jj % S);
+        RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
+        // the tile the new token goes to, its row count and the row it is written to
+        const bool is_slot = TOKD ? false : tok ? page == (slot >> 4) : page == slot;
+        const int patch = !is_slot ? -1 : (tok ? (slot & (PAGE - 1)) : off);
+        sinfo[2 * s] = make_int4(unit, page, (is_slot && !tok) ? off + 1 : c, patch);
+        sinfo[2 * s + 1] =
+            make_int4(kt, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
+        mbar_arrive_expect_tx(full(s), STAGE);  // tokd: the trailer comes with the page
+        bulk_load_hint(ring + s * STAGE, p.kvstore + (size_t)(unit * C + page) * p.pstr,
+                       STAGE, full(s), pol);
+      }
+      __syncwarp();
     };
     TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
     bool owned = false, owned_next = false;
@@ -763,6 +804,19 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     if (tile >= 0) fetch(tile);
     uint32_t j = 0;
     int k = 0;
+    int pre = 0;  // pages of the first tile issued before griddepcontrol.wait (early start)
+    if (early) {
+      if (tile >= 0) {
+        const int unit = tile / p.nsplit, p0 = (tile - unit * p.nsplit) * SP;
+        const int n = min(p0 + SP, nnatt) - p0;
+        if (n > 0) {
+          pre = min(n, BATCH);
+          issue_batch(0, pre, 0, unit, n, 0, ncnt, nphys, nplan.x, nplan.y & 0xffff);
+        }
+      }
+      pdl_wait();
+      pdl_launch_dependents();
+    }
     while (tile >= 0) {
       const int unit = tile / p.nsplit, split = tile - unit * p.nsplit;
       const int4 pl = nplan;
@@ -804,33 +858,14 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
         bulk_load(qbuf + par * Lay::QBUF, p.q + (size_t)unit * g * D, g * D * 2, qfull(par));
         if (n < NC) mbar_arrive_cnt(mfull(par), (NC - n) * 32);  // warps with no page here
       }
-      // pages in batches, one lane per page: each lane waits for its stage, fills the stage
-      // info and issues one 1-D bulk copy of the page (K rows then V rows, 16*D*4 contiguous
-      // bytes, stored pre-swizzled in HBM so they land bank-conflict-free for ldmatrix).  A batch never spans
-      // more than S positions: a parity wait must be at most one phase ahead of its barrier.
-      constexpr int BATCH = S < 32 ? S : 32;
-      for (int i0 = 0; i0 < n; i0 += BATCH) {
+      // the first tile's first batch may already be in flight (early start)
+      if (pre > 0) j += pre;
+      for (int i0 = pre; i0 < n; i0 += BATCH) {
         const int nb = min(BATCH, n - i0);
-        const int c = __shfl_sync(0xffffffffu, cntv, (i0 + lane) & 31);
-        const int page = __shfl_sync(0xffffffffu, physv, (i0 + lane) & 31);
-        if (lane < nb) {
-          const int i = i0 + lane;
-          const uint32_t jj = j + lane;
-          const int s = (int)(jj % S);
-          RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
-          // the tile the new token goes to, its row count and the row it is written to
-          const bool is_slot = TOKD ? false : tok ? page == (slot >> 4) : page == slot;
-          const int patch = !is_slot ? -1 : (tok ? (slot & (PAGE - 1)) : off);
-          sinfo[2 * s] = make_int4(unit, page, (is_slot && !tok) ? off + 1 : c, patch);
-          sinfo[2 * s + 1] =
-              make_int4(k, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
-          mbar_arrive_expect_tx(full(s), STAGE);  // tokd: the trailer comes with the page
-          bulk_load_hint(ring + s * STAGE, p.kvstore + (size_t)(unit * C + page) * p.pstr,
-                         STAGE, full(s), pol);
-        }
-        __syncwarp();
+        issue_batch(i0, nb, j, unit, n, k, cntv, physv, slot, off);
         j += nb;
       }
+      pre = 0;
       ++k;
     }
     for (int e = 0; e < NC; ++e, ++j) {  // one END sentinel per consumer
@@ -851,6 +886,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     dbg_add(8, t_start);
 #ifdef RAAS_DBG_TIMING
     if (lane == 0) g_raas_dbg[blockIdx.x][13] = dbg_gtimer();
+    if (lane == 0 && blockIdx.x < 256) g_raas_tl[p.dbg_slot & 7][blockIdx.x][2] = dbg_gtimer();
 #endif
   } else if (warp == 1) {
     // ============================ merge (per tile) ============================
@@ -1320,6 +1356,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
   // the last CTA out resets the dynamic-schedule counter for the next launch (which reads it
   // only after griddepcontrol.wait, i.e. after this grid has completed)
   __syncthreads();
+#ifdef RAAS_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_raas_tl[p.dbg_slot & 7][blockIdx.x][3] = dbg_gtimer();
+#endif
   if (threadIdx.x == 0) {
     const int done = atomicAdd(p.sched + 1, 1);
     if (done == (int)gridDim.x - 1) {

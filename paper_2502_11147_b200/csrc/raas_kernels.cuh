@@ -68,6 +68,9 @@ struct DecodeParams {
   const int32_t* vmap;   // [units][C] selected prompt pages of this step, ascending
   int table_scope;       // 0 per (request, kv-head) tables; 1 one table per request (D25)
   int n_kv;              // kv-heads per request (units of one request are consecutive)
+  int dbg_slot;          // RAAS_DBG_TIMING builds: timeline slot of this launch (0..7)
+  int early;             // 1: the previous kernel of the stream is not this handle's decode step,
+                         // so this handle's state may be read before griddepcontrol.wait
   uint32_t* req_x;       // [batch][C] table_scope 1: order-preserving max of the page scores
   int32_t* req_ctr;      // [batch]    table_scope 1: kv-heads of the request combined so far
   float scale_log2;  // softmax_scale * log2(e)

@@ -129,6 +129,17 @@ int main() {
       if (mode != 1) break;
     }
   }
+  // ring depth sweep (mode 0): bytes in flight per SM vs achieved bandwidth
+  for (int S : {8, 16, 24}) {  // multiples of the 8 consumers (a stage is always one warp's)
+    const int ch = 8192;
+    const int smem = S * ch + 2 * S * 8 + 64;
+    auto k = ring_stream<8>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const size_t nch = (bytes / ch) / (32 * sms) * (32 * sms);
+    double gbs = timeit([&] { k<<<sms, 9 * 32, smem>>>(a, nch, ch, S, 0, 32); });
+    gbs *= (double)(nch * ch) / bytes;
+    printf("ring 8K S=%d (%d KB in flight/SM): %.0f GB/s %s\n", S, S * 8, gbs, cudaGetErrorString(cudaGetLastError()));
+  }
   // launch-granular streaming: back-to-back launches over distinct 537 MB slices (the size of
   // one config-3 layer-step), the ceiling for a kernel that must stream that much per launch
   {

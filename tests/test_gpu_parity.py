@@ -612,3 +612,47 @@ def test_token_level_alpha_extremes(oracle_mod, alpha):
     for u in range(B * Hkv):
         assert set(s["start"][u][s["count"][u] > 0].tolist()) == want
     assert res.max_err <= OUT_TOL
+
+
+def test_interleaved_handles_early_start_matches_single_handle_runs():
+    """Layers interleaved on one stream (the model's order) take the early-start path: each
+    launch reads its handle's state before griddepcontrol.wait, since the previous kernel is
+    another handle's.  Outputs and states must be bitwise those of each handle stepped alone
+    (where every launch follows its own previous step and waits).  Eager and graph-captured."""
+    B, Hq, Hkv, d, P, T, L = 3, 8, 2, 128, 40, 120, 96
+    streams = [waterfall_stream(900 + i, B, Hq, Hkv, d, P, T) for i in range(3)]
+    ref = [_run_gpu(st, L, Hq, Hkv) for st in streams]
+    for use_graph in (False, True):
+        layers = []
+        for st in streams:
+            ly = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+            ly.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+            layers.append(ly)
+        qs = [[to_dev(x) for x in st.q] for st in streams]
+        ks = [[to_dev(x) for x in st.k] for st in streams]
+        vs = [[to_dev(x) for x in st.v] for st in streams]
+        outs = [[torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda") for _ in range(T)]
+                for _ in streams]
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+
+        def run():
+            for i in range(T):
+                for li, ly in enumerate(layers):
+                    ly.raas_decode_step(qs[li][i], ks[li][i], vs[li][i], outs[li][i], stream=s)
+
+        if use_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                run()
+            g.replay()
+        else:
+            with torch.cuda.stream(s):
+                run()
+        torch.cuda.synchronize()
+        for li, ly in enumerate(layers):
+            got = np.stack([from_dev(o) for o in outs[li]])
+            assert np.array_equal(got, ref[li][0]), (use_graph, li)
+            st_ = ly.raas_get_state()
+            assert all(np.array_equal(st_[k], ref[li][1][k]) for k in st_), (use_graph, li)
+            assert ly.raas_get_status() == 0
