@@ -788,7 +788,9 @@ int raas_launch_info(const raas_handle* h, int32_t info[5]) {
 #ifdef RAAS_DBG_TIMING
 // tuning experiment only (not part of the ABI in include/raas.h): read + clear the cycle counters
 RAAS_API int raas_debug_units(uint64_t* out, int n) {
-  RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg_unit, sizeof(uint64_t) * n));
+  RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg_unit, sizeof(uint64_t) * (n < 4096 * 4 ? n : 4096 * 4)));
+  if (n >= 4096 * 8)
+    RAAS_CUDA(cudaMemcpyFromSymbol(out + 4096 * 4, raas::g_raas_dbg_comb, sizeof(uint64_t) * 4096 * 4));
   return RAAS_OK;
 }
 RAAS_API int raas_debug_timeline(uint64_t* out, int n) {  // [8][256][4], then cleared

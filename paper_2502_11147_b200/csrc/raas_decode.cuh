@@ -34,6 +34,7 @@ namespace raas {
 #ifdef RAAS_DBG_TIMING  // tuning experiment: per-CTA cycle accounting of the pipeline waits
 __device__ unsigned long long g_raas_dbg[1024][16];
 __device__ unsigned long long g_raas_dbg_unit[4096][4];  // cta, pushed, combine start, end
+__device__ unsigned long long g_raas_dbg_comb[4096][4];  // combine phases: LSE done, out done, stamps done, end
 // multi-launch timeline: [launch slot][cta] = {entry, after griddepcontrol.wait, producer end, exit}
 __device__ unsigned long long g_raas_tl[8][256][4];
 __device__ __forceinline__ long long dbg_clock() { return clock64(); }
@@ -49,6 +50,12 @@ __device__ __forceinline__ unsigned long long dbg_gtimer() {
 __device__ __forceinline__ unsigned long long dbg_gtimer() { return 0; }
 __device__ __forceinline__ long long dbg_clock() { return 0; }
 __device__ __forceinline__ void dbg_add(int, long long) {}
+#endif
+#ifdef RAAS_DBG_TIMING
+#define RAAS_COMB_MARK(i) \
+  do { if (lane == 0 && unit < 4096) g_raas_dbg_comb[unit][i] = dbg_gtimer(); } while (0)
+#else
+#define RAAS_COMB_MARK(i) do {} while (0)
 #endif
 #define RAAS_TIMED(slot, stmt)          \
   do {                                  \
@@ -286,6 +293,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     sts_f32(scr_inv + 4 * lane, 1.f / L);
   }
   __syncwarp();
+  RAAS_COMB_MARK(0);
   float lse[MAX_GROUP];
 #pragma unroll
   for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
@@ -363,6 +371,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     }
   }
   // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
+  RAAS_COMB_MARK(1);
   if (tscope && !rq) return;  // another kv-head of the request decides
   if (rq) {
 #pragma unroll
@@ -440,9 +449,11 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       }
     }
   }
+  RAAS_COMB_MARK(2);
   const int victim = warp_argmin_page(best);
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
+  RAAS_COMB_MARK(3);
   if (lane == 0) {
     const int4 np = next_plan(slot, off + 1, used_eff, C, t, victim, p.status, GEN ? p.ep : PAGE);
     for (int r = 0; r < nrep; ++r) p.plan[unit0 + r] = np;
@@ -728,8 +739,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       const int unit = entry & ((1 << CQ_UNIT_BITS) - 1);
       const int nse_u = (entry >> CQ_UNIT_BITS) & ((CQ_OWNED >> CQ_UNIT_BITS) - 1);
       // partials of other SMs: released by their merge warps' acq_rel counter increments and
-      // acquired by ours before the push (CTA-scope handoff to us); read with ld.global.cg
-      if (!(entry & CQ_OWNED)) fence_acq_rel_gpu();
+      // acquired by our merge warp's (the same lane then pushes: mbarrier arrive = release.cta,
+      // our wait = acquire.cta).  Causality order is transitive, so no further fence is needed;
+      // the partials are read with ld.global.cg (L2, the point of coherence)
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif

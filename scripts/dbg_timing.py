@@ -75,14 +75,18 @@ print("producer end (us): min %.1f median %.1f max %.1f" % ((pe.min() - t0) / 1e
 print("combine end  (us): min %.1f median %.1f max %.1f" % ((ce.min() - t0) / 1e3, np.median(ce - t0) / 1e3, (ce.max() - t0) / 1e3))
 print("cycles/ns (SM clock GHz) ~ %.2f" % (buf[:g, 8].astype(np.float64).mean() / np.mean(pe - st)))
 
-ub = np.zeros((4096, 4), np.uint64)
+ub2 = np.zeros((2, 4096, 4), np.uint64)
 L_.raas_debug_units.argtypes = [ctypes.c_void_p, ctypes.c_int]
-L_.raas_debug_units(ub.ctypes.data_as(ctypes.c_void_p), ub.size)
-ub = ub[:U].astype(np.int64)
+L_.raas_debug_units(ub2.ctypes.data_as(ctypes.c_void_p), ub2.size)
+ub = ub2[0, :U].astype(np.int64)
+cm = ub2[1, :U].astype(np.int64)
 push, cs, ce = (ub[:, 1] - t0) / 1e3, (ub[:, 2] - t0) / 1e3, (ub[:, 3] - t0) / 1e3
 dur = ce - cs
 order = np.argsort(-ce)[:6]
 print("combine duration us: median %.1f max %.1f; queue delay median %.1f max %.1f" % (
     np.median(dur), dur.max(), np.median(cs - push), (cs - push).max()))
+ph = (cm - ub[:, 2:3]) / 1e3  # combine phase marks relative to the combine start
+print("combine phases (us from start, median): LSE %.2f  out %.2f  stamps %.2f  argmin %.2f  end %.2f" % (
+    *np.median(ph, 0), np.median(dur)))
 for u in order:
-    print(f"  unit {u}: cta {ub[u,0]} pushed {push[u]:.1f} start {cs[u]:.1f} end {ce[u]:.1f}")
+    print(f"  unit {u}: cta {ub[u,0]} pushed {push[u]:.1f} start {cs[u]:.1f} end {ce[u]:.1f}  phases {np.round(ph[u], 2)}")
