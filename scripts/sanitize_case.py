@@ -17,3 +17,31 @@ r4, _, _ = run_lockstep(oracle, st, L=96, alpha=1e-3, Hq=8, Hkv=2, split_pages=2
 r5, _, _ = run_lockstep(oracle, st, L=96, alpha=1e-3, Hq=8, Hkv=2, split_pages=2, page=1, table_scope=1)
 print("sanitize case ok", r1.max_err, r2.max_err, r3.max_err, r4.max_err, r5.max_err,
       r1.band_events + r2.band_events + r3.band_events + r4.band_events + r5.band_events)
+
+# early start (two handles interleaved on one stream) and the zero-copy host path
+import numpy as np, torch
+from paper_2502_11147_b200.raas import RaasLayer
+
+
+def bits_dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+sts = [waterfall_stream(20 + i, 2, 8, 2, 128, 40, 24) for i in range(2)]
+lys = []
+for st in sts:
+    ly = RaasLayer(96, 1e-4, 8, 2, 128, 2)
+    ly.raas_prefill(bits_dev(st.k_pre), bits_dev(st.v_pre), 40)
+    lys.append(ly)
+out = torch.empty((2, 8, 128), dtype=torch.bfloat16, device="cuda")
+for i in range(24):
+    for st, ly in zip(sts, lys):
+        ly.raas_decode_step(bits_dev(st.q[i]), bits_dev(st.k[i]), bits_dev(st.v[i]), out)
+pin = lambda x: torch.from_numpy(np.ascontiguousarray(x).view(np.int16)).view(torch.bfloat16).pin_memory()  # noqa: E731
+oh = torch.empty((2, 8, 128), dtype=torch.bfloat16).pin_memory()
+st = waterfall_stream(30, 2, 8, 2, 128, 40, 8)
+for i in range(8):
+    lys[0].raas_decode_step_host(pin(st.q[i]), pin(st.k[i]), pin(st.v[i]), oh)
+torch.cuda.synchronize()
+assert all(ly.raas_get_status() == 0 for ly in lys)
+print("sanitize early/host ok")

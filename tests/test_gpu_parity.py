@@ -397,7 +397,7 @@ def test_compute_sanitizer(tool):
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable, script],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "sanitize case ok" in r.stdout
+    assert "sanitize case ok" in r.stdout and "sanitize early/host ok" in r.stdout
     assert "ERROR SUMMARY: 0 errors" in r.stdout or "(0 errors, 0 warnings)" in r.stdout
 
 
