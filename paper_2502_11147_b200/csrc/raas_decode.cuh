@@ -69,7 +69,22 @@ constexpr int FLAG_LAST = 2;   // last page of this tile for the consuming warp
 constexpr int FLAG_END = 4;    // no more work
 constexpr int FLAG_SKIP = 8;   // padding position (keeps every tile aligned to the NC consumers)
 constexpr int CQ_OWNED = 1 << 30;  // combine-queue tag: all splits were processed by this CTA
-constexpr int CQ_UNIT_BITS = 20;   // entry = unit | nse << 20 | owned << 30
+constexpr int CQ_OUTDONE = 1 << 29;  // tag: the merge warp already wrote out; LSE in the slot
+constexpr int CQ_UNIT_BITS = 20;   // entry = unit | nse << 20 | outdone << 29 | owned << 30
+constexpr int CQ_NSE_MASK = (1 << 9) - 1;  // nse <= MAX_SPLITS < 512
+
+// The split combine (a5) is a running merge in split order, per head h and element d:
+//   m' = max(m, m_s);  f_a = 2^(m - m'), f_b = 2^(m_s - m')  (m' = -inf -> 0 in the exponent)
+//   l = l f_a + l_s f_b;  acc = acc f_a + acc_s f_b;  LSE = m + log2 l;  out = acc (1 / l).
+// The merge warp folds an owned unit's splits this way as they finish (no partials in HBM/L2),
+// the combine warp folds a shared unit's published partials the same way, with the same
+// operations, so a unit's result does not depend on which path (i.e. on the schedule) ran it.
+__device__ __forceinline__ void merge_factors(float m, float ms, float& mn, float& fa, float& fb) {
+  mn = fmaxf(m, ms);
+  const float sf = mn == -INFINITY ? 0.f : mn;
+  fa = fast_exp2(m - sf);
+  fb = fast_exp2(ms - sf);
+}
 
 // Tile schedule of one CTA (it never changes numerics: the split arithmetic is schedule-free).
 // With G CTAs, CTA b first streams the whole units [b*fu, (b+1)*fu), fu = units / G, whose
@@ -173,7 +188,8 @@ struct DecodeLayout {
   static constexpr int OFF_CQ = OFF_TINFO + 2 * 48;  // int[CQ] unit ids, then the pop counter
   // deferred token level (tokd): per stage the tile's 16 ts + 16 start values; per parity the
   // previous step's q and LSE; per (parity, consumer) the tile's victim candidate
-  static constexpr int OFF_TSB = (OFF_CQ + CQ * 4 + 32 + 127) / 128 * 128;
+  static constexpr int OFF_LSEQ = (OFF_CQ + CQ * 4 + 32 + 15) / 16 * 16;   // float[CQ][MAX_GROUP]
+  static constexpr int OFF_TSB = (OFF_LSEQ + CQ * MAX_GROUP * 4 + 127) / 128 * 128;
   static constexpr int OFF_CAND = OFF_TSB;
   static constexpr int OFF_QP = OFF_CAND + (TOKD ? 2 * NC * 16 : 0);
   static constexpr int QPBUF = QBUF + 32;  // q_prev rows, then 8 floats of LSE
@@ -196,7 +212,8 @@ struct DecodeLayout {
 // ---------------------------------------------------------------------------------------------
 template <int D, bool GEN>
 __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, int nse, uint32_t scr,
-                                             int lane) {
+                                             int lane, bool outdone) {
+  // outdone: the merge warp already folded the splits and wrote out; the LSE is in scr_lse
   // GEN = false: the default method (page = 16, alpha rule, one table per kv-head) with the
   // optional rules compiled out; GEN = true: every option decided at run time
   const bool tscope = GEN && p.table_scope != 0;
@@ -216,7 +233,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = 32 * k + lane;
-    mla[k] = i < NE ? __ldcg(ml_g + i) : make_float2(-INFINITY, 0.f);
+    mla[k] = (!outdone && i < NE) ? __ldcg(ml_g + i) : make_float2(-INFINITY, 0.f);
   }
   // page metadata for a6/a7 (bounded by C, masked by the plan's page count later)
   constexpr int PPL = 4;  // pages per lane per chunk
@@ -259,38 +276,41 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       const int c = lane + 32 * (cb + i), h = c / CPH, d4 = c - h * CPH;
 #pragma unroll
       for (int u = 0; u < SG; ++u)
-        v[i][u] = (c < nch && s0 + u < nse)
+        v[i][u] = (!outdone && c < nch && s0 + u < nse)
                       ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   load_acc(0, 0);
-  // ---- a5 (1): split maxima and sums -> per-head LSE and split weights ----
+  // ---- a5 (1): running merge of the split statistics -> per-split factors, LSE, 1 / l ----
+  if (!outdone) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int i = 32 * k + lane;
-    if (i < NE) { sts_f32(scr_w + 8 * i, mla[k].x); sts_f32(scr_w + 8 * i + 4, mla[k].y); }
-  }
-  for (int i = 64 + lane; i < NE; i += 32) {  // more than 64 (split, head) pairs
-    const float2 ml = __ldcg(ml_g + i);
-    sts_f32(scr_w + 8 * i, ml.x);
-    sts_f32(scr_w + 8 * i + 4, ml.y);
+    for (int k = 0; k < 2; ++k) {
+      const int i = 32 * k + lane;
+      if (i < NE) { sts_f32(scr_w + 8 * i, mla[k].x); sts_f32(scr_w + 8 * i + 4, mla[k].y); }
+    }
+    for (int i = 64 + lane; i < NE; i += 32) {  // more than 64 (split, head) pairs
+      const float2 ml = __ldcg(ml_g + i);
+      sts_f32(scr_w + 8 * i, ml.x);
+      sts_f32(scr_w + 8 * i + 4, ml.y);
+    }
   }
   const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
   const int used_eff = pl.z, t = pl.w;
   __syncwarp();
-  if (lane < g) {  // LSE_h = M + log2 sum_s 2^(m_s - M) l_s   (log2 domain)
-    float M = -INFINITY;
-    for (int s = 0; s < nse; ++s) M = fmaxf(M, lds_f32(scr_w + 8 * (s * g + lane)));
-    float L = 0.f;
+  if (!outdone && lane < g) {  // (m_s, l_s) of split s are replaced by its factors (f_a, f_b)
+    float m = -INFINITY, l = 0.f;
     for (int s = 0; s < nse; ++s) {
       const uint32_t a = scr_w + 8 * (s * g + lane);
-      const float w = fast_exp2(lds_f32(a) - M);
-      L += w * lds_f32(a + 4);
-      sts_f32(a, w);  // the split weight replaces m_s
+      float mn, fa, fb;
+      merge_factors(m, lds_f32(a), mn, fa, fb);
+      l = fmaf(l, fa, __fmul_rn(lds_f32(a + 4), fb));
+      m = mn;
+      sts_f32(a, fa);
+      sts_f32(a + 4, fb);
     }
-    sts_f32(scr_lse + 4 * lane, M + log2f(L));
-    sts_f32(scr_inv + 4 * lane, 1.f / L);
+    sts_f32(scr_lse + 4 * lane, m + log2f(l));
+    sts_f32(scr_inv + 4 * lane, 1.f / l);
   }
   __syncwarp();
   RAAS_COMB_MARK(0);
@@ -337,8 +357,8 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       load_meta(0, used_eff);
     }
   }
-  // ---- a5 (2): out[h][d] = sum_s w_s acc_s[h][d] / L_h ----
-  for (int cb = 0; 32 * cb < nch; cb += CB) {
+  // ---- a5 (2): out[h][d] = acc[h][d] / l_h, acc folded in split order ----
+  for (int cb = 0; !outdone && 32 * cb < nch; cb += CB) {
     float4 o[CB];
 #pragma unroll
     for (int i = 0; i < CB; ++i) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -351,9 +371,12 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
 #pragma unroll
           for (int u = 0; u < SG; ++u) {
             if (s0 + u < nse) {
-              const float w = lds_f32(scr_w + 8 * ((s0 + u) * g + h));
-              o[i].x += w * v[i][u].x; o[i].y += w * v[i][u].y;
-              o[i].z += w * v[i][u].z; o[i].w += w * v[i][u].w;
+              const uint32_t fa_a = scr_w + 8 * ((s0 + u) * g + h);
+              const float fa = lds_f32(fa_a), fb = lds_f32(fa_a + 4);
+              o[i].x = fmaf(o[i].x, fa, __fmul_rn(v[i][u].x, fb));
+              o[i].y = fmaf(o[i].y, fa, __fmul_rn(v[i][u].y, fb));
+              o[i].z = fmaf(o[i].z, fa, __fmul_rn(v[i][u].z, fb));
+              o[i].w = fmaf(o[i].w, fa, __fmul_rn(v[i][u].w, fb));
             }
           }
         }
@@ -652,6 +675,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
   const uint32_t base = (raw + 1023u) & ~1023u;  // 128B-swizzle atoms need 1024B alignment
   const uint32_t ring = base + Lay::OFF_RING, qbuf = base + Lay::OFF_Q;
   const uint32_t merge = base + Lay::OFF_MERGE, scr = base + Lay::OFF_SCR;
+  const uint32_t lseq = base + Lay::OFF_LSEQ;
   const uint32_t qpb = base + Lay::OFF_QP, cand = base + Lay::OFF_CAND;
   int4* sinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_SINFO);
   int4* tinfo = reinterpret_cast<int4*>(smem_raw + (base - raw) + Lay::OFF_TINFO);
@@ -734,10 +758,18 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       int entry = 0;
       if (lane == 0) entry = cq[q];
       entry = __shfl_sync(0xffffffffu, entry, 0);
+      const bool outdone = entry >= 0 && (entry & CQ_OUTDONE);
+      if (outdone && lane == 0) {  // the slot's LSE row -> this popper's scratch (the lane that
+        // releases the slot does every read of it)
+#pragma unroll
+        for (int h = 0; h < MAX_GROUP; ++h)
+          sts_f32(scratch + MAX_SPLITS * MAX_GROUP * 8 + 4 * h, lds_f32(lseq + 4 * (q * MAX_GROUP + h)));
+      }
+      __syncwarp();
       if (lane == 0) mbar_arrive(cqempty(q));  // the entry is read: the slot may be refilled
       if (entry < 0) break;
       const int unit = entry & ((1 << CQ_UNIT_BITS) - 1);
-      const int nse_u = (entry >> CQ_UNIT_BITS) & ((CQ_OWNED >> CQ_UNIT_BITS) - 1);
+      const int nse_u = (entry >> CQ_UNIT_BITS) & CQ_NSE_MASK;
       // partials of other SMs: released by their merge warps' acq_rel counter increments and
       // acquired by our merge warp's (the same lane then pushes: mbarrier arrive = release.cta,
       // our wait = acquire.cta).  Causality order is transitive, so no further fence is needed;
@@ -746,7 +778,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
       if constexpr (TOKD) combine_unit_tok<D>(p, unit, nse_u, scratch, lane);
-      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane);
+      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane, outdone);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -904,13 +936,26 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     // ============================ merge (per tile) ============================
     const int r = lane >> 2, qd = lane & 3;
     int npush = 0;
+    // running merge of the current owned unit's splits (heads 2qd, 2qd+1 of this lane)
+    float rm0 = -INFINITY, rm1 = -INFINITY, rl0 = 0.f, rl1 = 0.f, racc[KS * 4];
+#pragma unroll
+    for (int i = 0; i < KS * 4; ++i) racc[i] = 0.f;
+    float lse0 = 0.f, lse1 = 0.f;  // pushed with an outdone unit
     auto push = [&](int unit) {  // hand a finished unit (or -1 = END) to the combine warp
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit >= 0 && (unit & ((1 << CQ_UNIT_BITS) - 1)) < 4096) g_raas_dbg_unit[unit & ((1 << CQ_UNIT_BITS) - 1)][1] = dbg_gtimer();
 #endif
       const int q = npush % CQ;
       RAAS_TIMED(7, mbar_wait(cqempty(q), ((npush / CQ) & 1) ^ 1));
+      const bool od = unit >= 0 && (unit & CQ_OUTDONE);
+      float lv[MAX_GROUP];  // the unit's LSE per head, gathered to lane 0 (head h: lane h / 2)
+#pragma unroll
+      for (int h = 0; h < MAX_GROUP; ++h) lv[h] = __shfl_sync(0xffffffffu, (h & 1) ? lse1 : lse0, h >> 1);
       if (lane == 0) {
+        if (od) {
+#pragma unroll
+          for (int h = 0; h < MAX_GROUP; ++h) sts_f32(lseq + 4 * (q * MAX_GROUP + h), lv[h]);
+        }
         cq[q] = unit;
         mbar_arrive(cqfull(q));
       }
@@ -968,6 +1013,50 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       }
       __syncwarp();
       mbar_arrive(tfree(par));  // deposits / q / info of tile k consumed (each lane's reads)
+      if (!TOKD && owned) {
+        // an owned unit's splits arrive here in order on this CTA: fold the tile into the
+        // running merge; after the last split write out and hand the LSE to the combine
+        if (split == 0) {
+          rm0 = rm1 = -INFINITY;
+          rl0 = rl1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < KS * 4; ++i) racc[i] = 0.f;
+        }
+        float mn0, fa0, fb0, mn1, fa1, fb1;
+        merge_factors(rm0, M0, mn0, fa0, fb0);
+        merge_factors(rm1, M1, mn1, fa1, fb1);
+        rl0 = fmaf(rl0, fa0, __fmul_rn(L0, fb0));
+        rl1 = fmaf(rl1, fa1, __fmul_rn(L1, fb1));
+        rm0 = mn0;
+        rm1 = mn1;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          racc[4 * mt + 0] = fmaf(racc[4 * mt + 0], fa0, __fmul_rn(acc[4 * mt + 0], fb0));
+          racc[4 * mt + 1] = fmaf(racc[4 * mt + 1], fa1, __fmul_rn(acc[4 * mt + 1], fb1));
+          racc[4 * mt + 2] = fmaf(racc[4 * mt + 2], fa0, __fmul_rn(acc[4 * mt + 2], fb0));
+          racc[4 * mt + 3] = fmaf(racc[4 * mt + 3], fa1, __fmul_rn(acc[4 * mt + 3], fb1));
+        }
+        if (split == nse - 1) {
+          const float inv0 = 1.f / rl0, inv1 = 1.f / rl1;
+          lse0 = rm0 + log2f(rl0);
+          lse1 = rm1 + log2f(rl1);
+          __nv_bfloat16* o0 = p.out + (size_t)(unit * g + 2 * qd) * D + r;
+          __nv_bfloat16* o1 = o0 + D;
+#pragma unroll
+          for (int mt = 0; mt < KS; ++mt) {
+            if (2 * qd < g) {
+              o0[16 * mt] = __float2bfloat16_rn(racc[4 * mt + 0] * inv0);
+              o0[16 * mt + 8] = __float2bfloat16_rn(racc[4 * mt + 2] * inv0);
+            }
+            if (2 * qd + 1 < g) {
+              o1[16 * mt] = __float2bfloat16_rn(racc[4 * mt + 1] * inv1);
+              o1[16 * mt + 8] = __float2bfloat16_rn(racc[4 * mt + 3] * inv1);
+            }
+          }
+          push(unit | nse << CQ_UNIT_BITS | CQ_OWNED | CQ_OUTDONE);
+        }
+        continue;
+      }
       // publish the tile's split-K partial (m, l, acc) in the C-fragment layout
       const int pbase = (unit * p.nsplit + split) * g;
       if (TOKD && lane == 0) p.part_key[unit * p.nsplit + split] = ck;

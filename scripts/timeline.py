@@ -13,8 +13,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--B", type=int, default=64); ap.add_argument("--L", type=int, default=2048)
 ap.add_argument("--layers", type=int, default=8); ap.add_argument("--graph", type=int, default=1)
 ap.add_argument("--P", type=int, default=256); ap.add_argument("--sp", type=int, default=0)
+ap.add_argument("--Hq", type=int, default=32); ap.add_argument("--Hkv", type=int, default=8)
 a = ap.parse_args()
-B, Hq, Hkv, d, P, L = a.B, 32, 8, 128, a.P, a.L
+B, Hq, Hkv, d, P, L = a.B, a.Hq, a.Hkv, 128, a.P, a.L
 C, U = L // 16, B * Hkv
 Pp = -(-P // 16)
 meta = random_steady_state(77, U, C, Pp, Pp * 16 + 64 * (C - Pp) + 5)
@@ -51,7 +52,7 @@ order = np.argsort(x[:, :, 1].min(1))
 x = x[order]
 t0 = x[0, :, 1].min()
 r = (x - t0) / 1e3
-nb = U * (4 * d * (L - 7.5) + 4 * d + 4 * 4 * d + 12 * C)
+nb = U * (4 * d * (L - 7.5) + 4 * d + 4 * (Hq // Hkv) * d + 12 * C)
 print(f"grid {grid}; algorithmic bytes per launch {nb/1e6:.1f} MB")
 print("launch | entry min/max | release min/max | prod end min/med/max | exit min/med/max | busy(us) | GB/s")
 prev_exit = None
