@@ -58,10 +58,11 @@ def gather_heads(out_local, out_full=None):
     if dist.get_backend() == "nccl":
         stacked = torch.empty((world, B, hl, d), dtype=out_local.dtype, device=out_local.device)
         dist.all_gather_into_tensor(stacked, out_local.contiguous())
-    else:
-        parts = [torch.empty_like(out_local) for _ in range(world)]
-        dist.all_gather(parts, out_local.contiguous())
-        stacked = torch.stack(parts)
+    else:  # gloo (CPU tests, the bench's shared-GPU test mode): gather on the host
+        loc = out_local.contiguous().cpu()
+        parts = [torch.empty_like(loc) for _ in range(world)]
+        dist.all_gather(parts, loc)
+        stacked = torch.stack(parts).to(out_local.device)
     full = stacked.permute(1, 0, 2, 3).reshape(B, world * hl, d)
     if out_full is not None:
         out_full.copy_(full)
