@@ -292,7 +292,9 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
     const bool other = note_launch(h, st);  // always record the launch
     // the host path's ingest kernel waited for the previous kernel before triggering us
     static const bool no_early = std::getenv("RAAS_NO_EARLY") != nullptr;  // A/B experiments
-    p.early = (other || after_ingest) && !h->d.tokd && !h->d.gen && !no_early;
+    // not with the Quest-on-prefill hybrid: its selection kernel (this handle's) runs right
+    // before the decode kernel and writes the attended-page list the producer reads
+    p.early = (other || after_ingest) && h->cfg.quest_prefill_pages == 0 && !no_early;
   }
   p.n_kv = h->cfg.n_kv_heads;
   p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;

@@ -727,12 +727,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
                      : "memory");
     }
   }
-  // Early start (default method, p.early: the host saw that the previous kernel of the stream
+  // Early start (p.early: the host saw that the previous kernel of the stream
   // is not this handle's decode step): this handle's state was written by a kernel that
   // completed before the previous one could trigger us, so the producer reads its first tile's
   // metadata and issues that tile's first page copies BEFORE griddepcontrol.wait (below); only
   // the step's inputs (q, k_new, v_new) and every store wait for the previous kernel.
-  const bool early = !GEN && !TOKD && p.early != 0;
+  const bool early = p.early != 0;  // never with the Quest-on-prefill hybrid (host)
   if (!(early && warp == 0)) {
     pdl_wait();  // everything above overlapped the previous kernel; state reads start here
     pdl_launch_dependents();

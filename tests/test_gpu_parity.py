@@ -132,12 +132,12 @@ def test_dense_equivalence_gpu():
 # ------------------------------------------------------------------ determinism / sharding
 
 
-def _run_gpu(st, L, Hq, Hkv, batch_slice=None, split_pages=0):
+def _run_gpu(st, L, Hq, Hkv, batch_slice=None, split_pages=0, **kw):
     B, _, P, d = st.k_pre.shape
     sl = batch_slice if batch_slice is not None else slice(0, B)
     kp, vp = st.k_pre[sl], st.v_pre[sl]
     Bs = kp.shape[0]
-    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, Bs, split_pages=split_pages)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, Bs, split_pages=split_pages, **kw)
     layer.raas_prefill(to_dev(kp), to_dev(vp), P)
     out = torch.empty((Bs, Hq, d), dtype=torch.bfloat16, device="cuda")
     outs = []
@@ -614,18 +614,23 @@ def test_token_level_alpha_extremes(oracle_mod, alpha):
     assert res.max_err <= OUT_TOL
 
 
-def test_interleaved_handles_early_start_matches_single_handle_runs():
+@pytest.mark.parametrize("kw", [
+    {}, {"score_mode": 1}, {"stamp_rule": 1, "top_r": 0.5}, {"table_scope": 1},
+    {"page": 1}, {"page": 1, "stamp_rule": 1, "top_r": 0.5}, {"quest_prefill_pages": 1},
+], ids=["default", "quest", "top_r", "table", "token_tokd", "token_top_r", "hybrid"])
+def test_interleaved_handles_early_start_matches_single_handle_runs(kw):
     """Layers interleaved on one stream (the model's order) take the early-start path: each
     launch reads its handle's state before griddepcontrol.wait, since the previous kernel is
     another handle's.  Outputs and states must be bitwise those of each handle stepped alone
-    (where every launch follows its own previous step and waits).  Eager and graph-captured."""
+    (where every launch follows its own previous step and waits).  Eager and graph-captured,
+    for every kernel instantiation / method option."""
     B, Hq, Hkv, d, P, T, L = 3, 8, 2, 128, 40, 120, 96
     streams = [waterfall_stream(900 + i, B, Hq, Hkv, d, P, T) for i in range(3)]
-    ref = [_run_gpu(st, L, Hq, Hkv) for st in streams]
+    ref = [_run_gpu(st, L, Hq, Hkv, **kw) for st in streams]
     for use_graph in (False, True):
         layers = []
         for st in streams:
-            ly = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+            ly = RaasLayer(L, 1e-4, Hq, Hkv, d, B, **kw)
             ly.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
             layers.append(ly)
         qs = [[to_dev(x) for x in st.q] for st in streams]
