@@ -246,7 +246,7 @@ bool note_launch(const raas_handle* h, cudaStream_t st) {
 
 template <int D>
 int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* v_new,
-                  void* out, cudaStream_t st, bool after_ingest = false) {
+                  void* out, cudaStream_t st, bool after_copies = false) {
   DecodeParams p{};
   uint8_t* a = h->arena;
   p.q = static_cast<const __nv_bfloat16*>(q);
@@ -290,11 +290,13 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
 #endif
   {
     const bool other = note_launch(h, st);  // always record the launch
-    // the host path's ingest kernel waited for the previous kernel before triggering us
+    // after_copies: staged cudaMemcpyAsync copies precede this launch (full serialisation).
+    // The zero-copy ingest kernel triggers us at its start, so it does not count: the kernel
+    // two back has completed, the one right before (this handle's or not) may still run.
     static const bool no_early = std::getenv("RAAS_NO_EARLY") != nullptr;  // A/B experiments
     // not with the Quest-on-prefill hybrid: its selection kernel (this handle's) runs right
     // before the decode kernel and writes the attended-page list the producer reads
-    p.early = (other || after_ingest) && h->cfg.quest_prefill_pages == 0 && !no_early;
+    p.early = (other || after_copies) && h->cfg.quest_prefill_pages == 0 && !no_early;
   }
   p.n_kv = h->cfg.n_kv_heads;
   p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;
@@ -635,9 +637,10 @@ int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_
   }
   // pinned out: the combine stores the bf16 rows straight into host memory
   void* out = om ? om : a + h->lay.so;
+  const bool copies = !(qm && km && vm);
   int rc = h->cfg.head_dim == 128
-               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st, true)
-               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st, true);
+               ? launch_decode<128>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st, copies)
+               : launch_decode<64>(h, a + h->lay.sq, a + h->lay.sk, a + h->lay.sv, out, st, copies);
   if (rc) return rc;
   if (!om) RAAS_CUDA(cudaMemcpyAsync(out_host, a + h->lay.so, U * g * D * 2, cudaMemcpyDeviceToHost, st));
   return RAAS_OK;

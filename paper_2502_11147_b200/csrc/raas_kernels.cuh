@@ -490,7 +490,8 @@ __global__ void __launch_bounds__(QSEL_THREADS) raas_qselect_kernel(const __nv_b
 // read from host memory over PCIe by the SMs (zero-copy) and stored into the arena's staging
 // area.  The host reads are issued BEFORE griddepcontrol.wait (the host buffers are complete
 // when the call is made), so they overlap the previous kernel of the stream; the stores wait
-// for it (the staging area may still be read by this handle's previous step).  128-thread
+// for it (the staging area may still be read by this handle's previous step).  The decode
+// kernel is triggered at once, so its prologue overlaps the previous kernel's tail too.  128-thread
 // blocks with a small register budget fit beside a resident decode CTA.  Counts in 16 B
 // vectors; element i of the concatenation [q | k | v].
 constexpr int INGEST_THREADS = 128, INGEST_PER = 4;
@@ -508,6 +509,10 @@ __global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
     else if (i < nq + nkv) k_d[i - nq] = x;
     else v_d[i - nq - nkv] = x;
   };
+  // the decode step may start (its state reads and first page copies) at once: it reads q /
+  // k_new / v_new only after its own griddepcontrol.wait, i.e. after this grid has completed,
+  // and this grid completes only after the previous kernel of the stream (our wait below)
+  pdl_launch_dependents();
   uint4 r[INGEST_PER];
 #pragma unroll
   for (int j = 0; j < INGEST_PER; ++j) {
@@ -515,7 +520,6 @@ __global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
     if (i < total) r[j] = ld(i);
   }
   pdl_wait();
-  pdl_launch_dependents();
 #pragma unroll
   for (int j = 0; j < INGEST_PER; ++j) {
     const int i = tid + j * nth;
