@@ -140,6 +140,36 @@ int main() {
     gbs *= (double)(nch * ch) / bytes;
     printf("ring 8K S=%d (%d KB in flight/SM): %.0f GB/s %s\n", S, S * 8, gbs, cudaGetErrorString(cudaGetLastError()));
   }
+  // per-SM ceiling: fewer CTAs than SMs (config 4 at G = 128 streams on 128 SMs)
+  for (int G : {64, 96, 128, 136, 148}) {
+    for (int S : {16, 24}) {
+      const int ch = 8192;
+      const int smem = S * ch + 2 * S * 8 + 64;
+      auto k = ring_stream<8>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      const size_t nch = (bytes / ch) / (32 * G) * (32 * G);
+      double gbs = timeit([&] { k<<<G, 9 * 32, smem>>>(a, nch, ch, S, 0, 32); });
+      gbs *= (double)(nch * ch) / bytes;
+      printf("ring 8K S=%d grid=%d: %.0f GB/s = %.1f GB/s per CTA\n", S, G, gbs, gbs / G);
+    }
+  }
+  // launch-granular, config 4 size: 268 MB per launch (128 units x 2 MiB)
+  for (int G : {128, 148}) {
+    const size_t slice = 256ull << 20, nsl = bytes / slice;
+    const int ch = 8192, S = 16;
+    const int smem = S * ch + 2 * S * 8 + 64;
+    auto k = ring_stream<8>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEventRecord(e0);
+    const int N = 100;
+    for (int i = 0; i < N; ++i) k<<<G, 9 * 32, smem>>>(a + (i % nsl) * slice, slice / ch, ch, S, 0, 32);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("ring 8K S=16 grid=%d, 268 MB per launch, back-to-back: %.1f us/launch, %.0f GB/s\n", G,
+           ms / N * 1e3, slice / (ms / N * 1e-3) / 1e9);
+  }
   // launch-granular streaming: back-to-back launches over distinct 537 MB slices (the size of
   // one config-3 layer-step), the ceiling for a kernel that must stream that much per launch
   {
