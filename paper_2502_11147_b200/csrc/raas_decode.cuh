@@ -1414,12 +1414,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       const float p2 = fast_exp2(s2 - mb0), p3 = fast_exp2(s3 - mb1);
       l0 = l0 * cr0 + (p0 + p2);
       l1 = l1 * cr1 + (p1 + p3);
+      // rescale only when some head's running max moved (x * 1 = x: bitwise the same result)
+      if (!__all_sync(0xffffffffu, cr0 == 1.f && cr1 == 1.f)) {
 #pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
-        acc[mt][0] *= cr0;
-        acc[mt][1] *= cr1;
-        acc[mt][2] *= cr0;
-        acc[mt][3] *= cr1;
+        for (int mt = 0; mt < KS; ++mt) {
+          acc[mt][0] *= cr0;
+          acc[mt][1] *= cr1;
+          acc[mt][2] *= cr0;
+          acc[mt][3] *= cr1;
+        }
       }
       // P^T as the B operand of O^T = V^T P^T: transpose the two 8x8 bf16 blocks in registers
       const uint32_t b0 = movmatrix_t(pack_bf16x2(p0, p1));
