@@ -137,21 +137,32 @@ __device__ __forceinline__ unsigned long long warp_kth_largest(uint32_t keys, ui
     const int excl = incl - tot;
     const unsigned hit = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
     const int src = __ffs(hit) - 1;
-    int digit = 0, above = 0;
+    int digit = 0, above = 0, csel = 0;
     if (lane == src) {
       int run = excl;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (run + c[j] >= krem) { digit = 255 - (lane * 8 + j); above = run; break; }
+        if (run + c[j] >= krem) { digit = 255 - (lane * 8 + j); above = run; csel = c[j]; break; }
         run += c[j];
       }
     }
     digit = __shfl_sync(0xffffffffu, digit, src);
     above = __shfl_sync(0xffffffffu, above, src);
+    csel = __shfl_sync(0xffffffffu, csel, src);
     krem -= above;
     prefix |= static_cast<unsigned long long>(digit) << shift;
     mask |= 255ull << shift;
     __syncwarp();
+    if (csel == 1 && shift > 0) {  // one key left in the selected bucket: it is the k-th largest
+      unsigned long long hitkey = 0;
+      for (int i = lane; i < n; i += 32) {
+        unsigned long long key;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(key) : "r"(keys + 8 * i));
+        if (key != 0 && (key & mask) == prefix) hitkey = key;
+      }
+      const unsigned who = __ballot_sync(0xffffffffu, hitkey != 0);
+      return __shfl_sync(0xffffffffu, hitkey, __ffs(who) - 1);
+    }
   }
   return prefix;
 }

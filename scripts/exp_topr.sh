@@ -1,0 +1,7 @@
+#!/bin/bash
+# top-r rule: radix select with early exit vs base
+q() { RAAS_LIB=$1 python bench.py --no-e2e --no-cpu-baseline "${@:2}" 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$(basename $1 .so)', '${*:2}', round(d['roofline']['achieved']), 'GB/s', round(d['roofline']['avg_launch_us'],2), 'us', d['clocks']['sm_mhz'])"; }
+for rep in 1 2; do for f in "$@"; do
+  q $f --steps 100 --top-r 0.5
+  q $f --steps 60 --top-r 0.5 --page 1
+done; done
