@@ -1,0 +1,6 @@
+#!/bin/bash
+# Quest page-score mode (score_mode 1): builds A/B at config 3
+q() { RAAS_LIB=$1 python bench.py --no-e2e --no-cpu-baseline "${@:2}" 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$(basename $1 .so)', '${*:2}', round(d['roofline']['achieved']), 'GB/s', round(d['roofline']['avg_launch_us'],2), 'us', d['clocks']['sm_mhz'])"; }
+for rep in 1 2; do for f in "$@"; do
+  q $f --steps 100 --score quest
+done; done
