@@ -820,7 +820,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     // bytes, stored pre-swizzled in HBM so they land bank-conflict-free for ldmatrix).  A batch
     // never spans more than S positions: a parity wait must be at most one phase ahead of its
     // barrier.
-    constexpr int BATCH = S < 32 ? S : 32;
+    // Half a ring per batch: a batch's lanes reconverge after their empty waits, so a batch is
+    // issued when its LAST stage frees; with whole-ring batches the ring drained before each
+    // refill (config 4: 48.9 -> 46.7 us per launch with S / 2, config 3 -1.5 %; S / 4 and single
+    // pages are slower; pre-issuing a whole ring at early start instead of one batch: no gain)
+#ifndef RAAS_BATCH
+    constexpr int BATCH = S / 2 < 32 ? S / 2 : 32;
+#else
+    constexpr int BATCH = RAAS_BATCH;
+#endif
     auto issue_batch = [&](int i0, int nb, uint32_t jb, int unit, int n, int kt, int cntv, int physv,
                            int slot, int off) {
       const int c = __shfl_sync(0xffffffffu, cntv, (i0 + lane) & 31);
