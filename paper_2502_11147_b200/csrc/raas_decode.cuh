@@ -266,7 +266,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   load_meta(0, C);
   // first block of split partials: 4 float4 chunks per lane x 2 splits
   constexpr int CPH = D / 4;                   // chunks per head
-  constexpr int CB = 4, SG = 4;
+  constexpr int CB = 4, SG = 2;
   const int nch = g * CPH;
   const float* acc_g = p.part_acc + (size_t)unit * p.nsplit * g * D;
   float4 v[CB][SG];
