@@ -443,6 +443,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if rank != 0:
         return None
+    cache_bytes = nl * 2 * units * C * 16 * d * 2  # this rank's K/V stores over the layer handles
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
@@ -451,7 +452,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     out = {
         "metric": METRIC,
         "value": value,
-        "unit": f"decode steps/s (model steps: {B} requests x {nl} layers per GPU per step, summed over GPUs)",
+        "unit": (f"decode steps/s (model steps: {B} requests x {nl} layers, kv-heads split over {world} GPUs)"
+                 if heads else
+                 f"decode steps/s (model steps: {B} requests x {nl} layers per GPU per step, summed over GPUs)"),
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -465,7 +468,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                  "on the GPU, bf16, a distinct input per step" if args.data == "waterfall" else
                  "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)"),
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
-                   "per_gpu_batch": B, "global_batch": B * world, "prefill": P, "L": L,
+                   "per_gpu_batch": B, "global_batch": B if heads else B * world, "prefill": P, "L": L,
                    "page": args.page, "alpha": args.alpha, "score_mode": args.score,
                    "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
                    "quest_prefill_pages": args.quest_prefill,
@@ -473,8 +476,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "variant": variant_name(args),
                    "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
                                    if heads else f"request-sharded x{world}, no collective"),
-                   "l2": f"{nl} distinct layer caches = {nl * 2 * units * C * 16 * d * 2 / 2**30:.2f} GiB "
-                         "> 126 MB L2 (no flush needed)",
+                   "l2": (f"{nl} distinct layer caches = {cache_bytes / 2**30:.2f} GiB "
+                          + ("> 126 MB L2 (no flush needed)" if cache_bytes > 126e6 else
+                             "< 126 MB L2: part of the K/V stream can hit in L2")),
                    "steady_state": f"{fill_steps} decode steps before warmup (all pages used, evicting)"},
         "tokens_per_s": value * B,
         "achieved_note": ("per-GPU HBM figures; the roofline covers this rank's decode launches"
