@@ -720,7 +720,11 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     const int fu = p.units / (int)gridDim.x;
     if (fu > 0) {
       const int unit0 = blockIdx.x * fu;
-      for (int pg = lane; pg < min(RAAS_PREFETCH_TILES * p.split_pages, fu * p.C); pg += 32)
+      // about an eighth of the CTA's owned tiles, 1..RAAS_PREFETCH_TILES (config 3, 12 owned
+      // tiles: 2; config 4 and the small budgets, 4-8: 1; measured per config, see
+      // profiles/r01_schedule_study.md)
+      const int npf = min(RAAS_PREFETCH_TILES, max(1, (fu * p.nsplit + 4) / 8));
+      for (int pg = lane; pg < min(npf * p.split_pages, fu * p.C); pg += 32)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
                          p.kvstore + ((size_t)unit0 * p.C + pg) * p.pstr),  // unit-major
                      "r"(p.pstr * 2)

@@ -1,0 +1,9 @@
+#!/bin/bash
+# L2 prefetch depth (tiles warmed before griddepcontrol.wait) and split size, after the half-ring batches
+q() { RAAS_LIB=$1 python bench.py --no-e2e --no-cpu-baseline "${@:2}" 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$(basename $1 .so)', '${*:2}', round(d['roofline']['achieved']), 'GB/s', round(d['roofline']['avg_launch_us'],2), 'us', d['clocks']['sm_mhz'])"; }
+for rep in 1 2; do for f in "$@"; do
+  q $f --steps 100
+  q $f --config 4 --steps 60
+  q $f --config 5 --L 512 --layers 8 --steps 100
+done; done
+for sp in 64 16; do q build_exp/libraas_base.so --steps 100 --split-pages $sp; q build_exp/libraas_base.so --config 4 --steps 60 --split-pages $sp; done
