@@ -26,7 +26,7 @@
 #pragma once
 
 #ifndef RAAS_PREFETCH_TILES
-#define RAAS_PREFETCH_TILES 2  // owned tiles warmed in L2 before griddepcontrol.wait
+#define RAAS_PREFETCH_TILES 4  // cap on the owned tiles warmed in L2 before griddepcontrol.wait
 #endif
 
 namespace raas {
@@ -721,8 +721,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
     if (fu > 0) {
       const int unit0 = blockIdx.x * fu;
       // about an eighth of the CTA's owned tiles, 1..RAAS_PREFETCH_TILES (config 3, 12 owned
-      // tiles: 2; config 4 and the small budgets, 4-8: 1; measured per config, see
-      // profiles/r01_schedule_study.md)
+      // tiles: 2; config 4 and the small budgets, 4-8: 1; L = 4096 / 8192, 24 / 48: 3 / 4;
+      // measured per config, see profiles/r01_schedule_study.md)
       const int npf = min(RAAS_PREFETCH_TILES, max(1, (fu * p.nsplit + 4) / 8));
       for (int pg = lane; pg < min(npf * p.split_pages, fu * p.C); pg += 32)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
