@@ -2,12 +2,19 @@
 """bench.py — RaaS decode hot path on B200 (libraas), driver contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+                    [--scaling weak|strong] [--shard requests|heads]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+`--gpus N` without torchrun (WORLD_SIZE unset) launches the N ranks itself (one process per
+GPU, NCCL rendezvous on 127.0.0.1); under torchrun `--gpus` must equal WORLD_SIZE.
 
 A "step" is one MODEL decode step: `layers` raas_decode_step launches (one per layer handle,
 each a distinct 512 MiB KV cache at the headline config), i.e. every row of SURVEY.md §8(a)
-for every request of this rank's batch.  Requests are sharded over ranks (weak scaling: a
-fixed per-GPU batch), with no collective on the hot path.
+for every request of this rank's batch.  Requests are sharded over ranks with no collective on
+the hot path: `--scaling weak` (default) keeps the per-GPU batch fixed,
+`--scaling strong` splits the config's global batch (config 4: 256 requests) over the ranks.
+`--shard heads` splits the kv-heads instead (config 2, B = 1) with one NCCL all-gather of out
+per layer-step, captured with the decode launches in one CUDA graph.
 
 Rank 0 prints ONE JSON line.  `value` = model decode steps/s summed over GPUs (each step
 decodes `per_gpu_batch` tokens per GPU); `e2e` = the same metric through
@@ -41,14 +48,64 @@ CONFIGS = {
             hq=32, hkv=8, d=128, layers=32, batch=64, P=256, L=2048, decode=16384),
     4: dict(workload="r1_distill_qwen7b_b32pergpu_L4096",
             model="DeepSeek-R1-Distill-Qwen-7B attention (28q/4kv, d=128)", hq=28, hkv=4, d=128,
-            layers=28, batch=32, P=128, L=4096, decode=32768),
+            layers=28, batch=32, global_batch=256, P=128, L=4096, decode=32768),
     5: dict(workload="llama31_8b_b64_budget_sweep", model="Llama-3.1-8B attention (32q/8kv, d=128)",
             hq=32, hkv=8, d=128, layers=4, batch=64, P=128, L=2048, decode=32768),
 }
 
 
+UNIT = "decode steps/s"  # both arms (ours, --impl reference) print exactly this unit
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def unit_detail(B, nl, world, mode):
+    """What one 'decode step' is in this run (the unit string itself is UNIT for every arm)."""
+    if mode == "heads":
+        return f"model steps of {B} request(s) x {nl} layers, kv-heads split over {world} GPUs"
+    if mode == "strong":
+        return f"model steps of the global batch ({B} requests over {world} GPUs) x {nl} layers"
+    return f"model steps of {B} requests x {nl} layers per GPU, summed over {world} GPU(s)"
+
+
+def free_port():
+    import socket
+
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    return port
+
+
+def spawn_ranks(n, argv):
+    """`--gpus N` without torchrun: start N ranks of this script (RANK / LOCAL_RANK /
+    WORLD_SIZE / MASTER_* set as torchrun would, rendezvous on 127.0.0.1); rank 0's stdout is
+    this process's.  A failing rank stops the others.  Returns the exit code."""
+    import subprocess
+
+    port = free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    while procs:
+        for p_ in list(procs):
+            code = p_.poll()
+            if code is None:
+                continue
+            procs.remove(p_)
+            if code != 0:
+                rc = rc or code
+                for q_ in procs:
+                    q_.kill()
+        time.sleep(0.05)
+    return rc
 
 
 # ----------------------------------------------------------------------------------- clocks
@@ -217,12 +274,20 @@ def oracle_sample(cfg, seconds=12.0, max_steps=100000, seed=4242):
 
 
 # ----------------------------------------------------------------------------------- main arm
+def l2_rotation(cache_bytes_per_rot, l2_bytes, cap=64):
+    """Distinct layer-cache sets cycled by consecutive steps so that the caches one step's
+    timing can hit in L2 are >= 4x the L2 size (SURVEY §8(d) L2 hygiene); capped (toy)."""
+    need = 4 * l2_bytes
+    return max(1, min(cap, -(-need // max(1, cache_bytes_per_rot))))
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import numpy as np
     import torch
 
     from paper_2502_11147_b200 import build as build_mod
     from paper_2502_11147_b200.raas import RaasLayer
+    from paper_2502_11147_b200.shard import HeadGather, head_range, request_range
 
     if rank == 0 or not os.path.exists(build_mod.LIB):
         build_mod.build()
@@ -230,57 +295,72 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.distributed.barrier()
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    B, hq, hkv, d, L, P, nl = cfg["batch"], cfg["hq"], cfg["hkv"], cfg["d"], cfg["L"], cfg["P"], cfg["layers"]
-    g = hq // hkv
+    hq, hkv, d, L, P, nl = cfg["hq"], cfg["hkv"], cfg["d"], cfg["L"], cfg["P"], cfg["layers"]
     heads = args.shard == "heads" and world > 1
+    mode = "heads" if heads else args.scaling
     if heads and args.table_scope:
         raise SystemExit("--table-scope 1 shares one page table over a request's kv-heads; "
                          "shard by requests")
+    B_global = cfg.get("global_batch", cfg["batch"]) if mode == "strong" else cfg["batch"] * world
+    if mode == "strong":
+        b_lo, b_hi = request_range(B_global, world, rank)
+        B = b_hi - b_lo
+        if B == 0:
+            raise SystemExit(f"strong scaling: {B_global} requests leave rank {rank} idle")
+    else:
+        B = cfg["batch"]
+    g = hq // hkv
     hq_full = hq
     if heads:  # this rank's kv-heads and their q-heads; out is all-gathered every layer-step
-        from paper_2502_11147_b200.shard import gather_heads, head_range
-
         kv_lo, kv_hi, q_lo, q_hi = head_range(hkv, hq, world, rank)
         hkv, hq = kv_hi - kv_lo, q_hi - q_lo
     C = L // 16
     Pp = -(-P // 16)
     units = B * hkv
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000 * args.config + rank)
     sp = args.split_pages if args.split_pages else cfg.get("split_pages", 0)
     score_mode = 1 if args.score == "quest" else 0
+    # L2 hygiene: enough distinct layer-cache sets that consecutive steps never re-read L2
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    set_bytes = nl * 2 * units * C * 16 * d * 2
+    rot = l2_rotation(set_bytes, l2) if args.rotate < 0 else max(1, args.rotate)
     layers = [RaasLayer(L, args.alpha, hq, hkv, d, B, device=dev, split_pages=sp, score_mode=score_mode,
                         stamp_rule=1 if args.top_r > 0 else 0, top_r=args.top_r,
                         quest_prefill_pages=args.quest_prefill, table_scope=args.table_scope,
                         page=args.page)
-              for _ in range(nl)]
+              for _ in range(nl * rot)]
+    lay = lambda r: layers[r * nl:(r + 1) * nl]  # noqa: E731  (rotation r's layer handles)
     info = layers[0].raas_launch_info()
     # steady state before the timed region: fill the decode pages once, then a further page cycle
     fill_steps = (C - Pp) * 16 + 256 if args.fill < 0 else args.fill
     fill_steps = min(fill_steps, cfg["decode"])
     e_steps = max(4, min(args.steps, 64))
-    R = args.warmup + args.steps  # one distinct input slot (and graph) per warmup/timed step
+    # one distinct input slot (and graph) per warmup/timed step; slot s runs rotation s % rot
+    R = -(-(args.warmup + args.steps) // rot) * rot
     if args.data == "gaussian":
-        R = 8  # i.i.d. inputs: a small ring suffices
+        R = max(8, rot)  # i.i.d. inputs: a small ring suffices
     qs = [torch.empty((B, hq, d), device=dev, dtype=torch.bfloat16) for _ in range(R)]
     ks = [torch.empty((B, hkv, d), device=dev, dtype=torch.bfloat16) for _ in range(R)]
     vs = [torch.empty((B, hkv, d), device=dev, dtype=torch.bfloat16) for _ in range(R)]
     stream = torch.cuda.Stream(device=dev)
+    seed = 1000 * args.config + rank
     if args.data == "waterfall":
-        # PAPER.md §3.1 waterfall workload, drawn on the GPU step by step; every
-        # layer sees the same stream (distinct caches, identical contents)
+        # PAPER.md §3.1 waterfall workload, drawn on the GPU step by step; each
+        # rotation is its own stream (every layer of it sees the same draws: distinct caches)
         from paper_2502_11147_b200.synth import WaterfallTorch
 
-        wf = WaterfallTorch(1000 * args.config + rank, B, hq, hkv, d, P,
-                            fill_steps + R + e_steps + 8, dev, lam=args.lam)
+        wfs = [WaterfallTorch(seed + 7919 * r, B, hq, hkv, d, P, fill_steps + R + e_steps + 8, dev,
+                              lam=args.lam) for r in range(rot)]
         with torch.cuda.stream(stream):
-            k, v = wf.prefill()
-            for ly in layers:
-                ly.raas_prefill(k, v, P, stream=stream)
+            for r in range(rot):
+                k, v = wfs[r].prefill()
+                for ly in lay(r):
+                    ly.raas_prefill(k, v, P, stream=stream)
         stream.synchronize()
         del k, v
-        draw = lambda s_: wf.step(qs[s_], ks[s_], vs[s_])  # noqa: E731
+        draw = lambda s_: wfs[s_ % rot].step(qs[s_], ks[s_], vs[s_])  # noqa: E731
     else:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
         for ly in layers:
             k = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
             v = torch.randn((B, hkv, P, d), device=dev, generator=gen).bfloat16()
@@ -292,29 +372,31 @@ def run_ours(args, cfg, rank, world, local_rank):
             vs[s_].copy_(torch.randn((B, hkv, d), device=dev, generator=gen))
         draw = lambda s_: None  # noqa: E731
     outs = [torch.empty((B, hq, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)]
-    outs_full = [torch.empty((B, hq_full, d), device=dev, dtype=torch.bfloat16) for _ in range(nl)] if heads else None
+    gathers = [HeadGather(B, hq, d, torch.bfloat16, dev) for _ in range(nl)] if heads else None
 
-    def eager_step(s_):  # head-sharded: decode, then the per-layer NCCL all-gather of out
-        for li, ly in enumerate(layers):
+    def model_step(s_):  # one model step on input slot s_: nl launches (+ nl all-gathers)
+        for li, ly in enumerate(lay(s_ % rot)):
             ly.raas_decode_step(qs[s_], ks[s_], vs[s_], outs[li], stream=stream)
-            gather_heads(outs[li], outs_full[li])
+            if heads:
+                gathers[li](outs[li])
 
-    # one CUDA graph per input slot, each = one model step (nl decode launches)
+    # one CUDA graph per input slot, each = one model step (head sharding over NCCL: the
+    # all-gathers are captured with the launches; gloo test mode runs eagerly)
+    graphed = not heads or gathers[0].capturable
     graphs = []
     torch.cuda.synchronize()
-    if not heads:
+    if graphed:
         with torch.cuda.stream(stream):
             for s in range(R):
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gr, stream=stream):
-                    for li, ly in enumerate(layers):
-                        ly.raas_decode_step(qs[s], ks[s], vs[s], outs[li], stream=stream)
+                    model_step(s)
                 graphs.append(gr)
-    run_step = (lambda s_: eager_step(s_)) if heads else (lambda s_: graphs[s_].replay())
-    # capturing does not execute; fill now (real steps)
+    run_step = (lambda s_: graphs[s_].replay()) if graphed else model_step
+    # capturing does not execute; fill now (real steps; every rotation advances fill_steps)
     t_fill = time.perf_counter()
     with torch.cuda.stream(stream):  # CUDAGraph.replay() launches on the current stream
-        for i in range(fill_steps):
+        for i in range(fill_steps * rot):
             draw(i % R)
             run_step(i % R)
     torch.cuda.synchronize()
@@ -322,8 +404,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     c0 = [ly.raas_get_counters() for ly in layers]
     st0 = layers[0].raas_get_state()
     Ce = L // args.page  # state entries per unit: pages, or token slots (page = 1)
-    log(f"[rank {rank}] filled {fill_steps} model steps in {t_fill:.1f}s; used entries/unit="
-        f"{(st0['count'] > 0).sum(1).mean():.1f}/{Ce}; launch {info}")
+    log(f"[rank {rank}] filled {fill_steps} model steps x {rot} rotation(s) in {t_fill:.1f}s; used "
+        f"entries/unit={(st0['count'] > 0).sum(1).mean():.1f}/{Ce}; batch {B}; launch {info}")
 
     # the warmup and timed steps' inputs, drawn before the timed region (slot i = step i)
     with torch.cuda.stream(stream):
@@ -351,16 +433,19 @@ def run_ours(args, cfg, rank, world, local_rank):
             torch.distributed.barrier()
     ms = ev0.elapsed_time(ev1)
     red_dev = dev if not world > 1 or torch.distributed.get_backend() == "nccl" else "cpu"
-    t_max = torch.tensor([ms], device=red_dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    per_rank = [ms]
+    if world > 1:  # max over ranks (and every rank's own time, to show all ranks worked)
+        t_all = torch.zeros(world, device=red_dev, dtype=torch.float64)
+        t_all[rank] = ms
+        torch.distributed.all_reduce(t_all)
+        per_rank = [float(x) for x in t_all.cpu()]
+    ms_max = max(per_rank)
     ms_per_step = ms_max / args.steps
     c1 = [ly.raas_get_counters() for ly in layers]
-    stamps = sum(b["stamps"] - a["stamps"] for a, b in zip(c0, c1))
-    decisions = sum(b["decisions"] - a["decisions"] for a, b in zip(c0, c1))
-    evictions = sum(b["evictions"] - a["evictions"] for a, b in zip(c0, c1))
-    unit_steps = sum(b["unit_steps"] - a["unit_steps"] for a, b in zip(c0, c1))
+    stamps = sum(b_["stamps"] - a_["stamps"] for a_, b_ in zip(c0, c1))
+    decisions = sum(b_["decisions"] - a_["decisions"] for a_, b_ in zip(c0, c1))
+    evictions = sum(b_["evictions"] - a_["evictions"] for a_, b_ in zip(c0, c1))
+    unit_steps = sum(b_["unit_steps"] - a_["unit_steps"] for a_, b_ in zip(c0, c1))
     status = max(ly.raas_get_status() for ly in layers)
 
     # algorithmic bytes per launch: K+V of resident tokens (steady state: the
@@ -382,7 +467,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce)
     variant = bool(args.score != "exact" or args.top_r > 0 or args.table_scope or args.page != 16
                    or args.quest_prefill or args.P or args.L or args.batch or args.layers
-                   or args.split_pages or args.dense or heads)
+                   or args.split_pages or args.dense or heads or mode == "strong")
     launch_s = ms_per_step / 1e3 / nl
     achieved = bytes_launch / launch_s / 1e9
     peak, peak_src = measured_peaks()
@@ -390,7 +475,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         raise RuntimeError(f"achieved {achieved:.0f} GB/s > 1.3x the copy peak: the timed region "
                            "did not do the work")
     model_steps_per_s = args.steps / (ms_max / 1e3)
-    value = model_steps_per_s * (1 if heads else world)  # head sharding: all ranks, one batch
+    # weak: every GPU steps its own batch -> summed; strong / heads: one global step per period
+    value = model_steps_per_s * (world if mode == "weak" else 1)
+    tokens_per_s = model_steps_per_s * (B * world if mode == "weak" else B_global if mode == "strong" else B)
 
     # ---------------- e2e: through raas_decode_step_host with pinned host buffers -------
     e2e = None
@@ -414,7 +501,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         def e2e_step():  # one stream: H2D, step, D2H of every layer in order (no overlap)
             j = e_next[0]
             e_next[0] += 1
-            for li, ly in enumerate(layers):
+            for li, ly in enumerate(lay(j % rot)):
                 ly.raas_decode_step_host(hq_[j], hk_[j], hv_[j], ho_[li], stream=stream)
 
         for _ in range(2):
@@ -435,32 +522,34 @@ def run_ours(args, cfg, rank, world, local_rank):
         te = torch.tensor([e_ms], device=red_dev, dtype=torch.float64)
         if world > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": e_steps / (float(te.item()) / 1e3) * world,
-               "unit": "decode steps/s", "steps": e_steps,
-               "h2d_bytes_per_step": nl * (B * hq * d + 2 * B * hkv * d) * 2,
-               "d2h_bytes_per_step": nl * B * hq * d * 2,
+        e2e = {"value": e_steps / (float(te.item()) / 1e3) * (world if mode == "weak" else 1),
+               "unit": UNIT, "steps": e_steps,
+               "h2d_bytes_per_step": nl * (B * hq * d + 2 * B * hkv * d) * 2 * world,
+               "d2h_bytes_per_step": nl * B * hq * d * 2 * world,
                "api": "raas_decode_step_host (pinned host q/k_new/v_new -> out: zero-copy ingest kernel + out stored to host by the combine), one stream, layers in order"}
 
     if rank != 0:
         return None
-    cache_bytes = nl * 2 * units * C * 16 * d * 2  # this rank's K/V stores over the layer handles
+    cache_bytes = rot * set_bytes  # this rank's K/V stores over all layer handles
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
-        cpu = {"value": ups / (units * nl), "unit": "decode steps/s", "cores": threads,
+        cpu = {"value": ups / (units * nl), "unit": UNIT, "cores": threads,
                "kind": "oracle", "sample": desc, "unit_steps_per_s": ups}
+    l2_note = (f"{nl * rot} distinct layer caches ({rot} rotation(s) of {nl}) = "
+               f"{cache_bytes / 2**30:.3f} GiB vs L2 {l2 / 2**20:.0f} MiB: "
+               + (f">= 4x L2, consecutive steps read disjoint caches (no flush needed)"
+                  if cache_bytes >= 4 * l2 else "< 4x L2: part of the K/V stream can hit in L2"))
     out = {
         "metric": METRIC,
         "value": value,
-        "unit": (f"decode steps/s (model steps: {B} requests x {nl} layers, kv-heads split over {world} GPUs)"
-                 if heads else
-                 f"decode steps/s (model steps: {B} requests x {nl} layers per GPU per step, summed over GPUs)"),
+        "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong" if heads else "weak",
+        "scaling": "weak" if mode == "weak" else "strong",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": (f"synthetic waterfall stream (PAPER.md §3.1 / DESIGN.md §4: sink + 2 recent pages, "
@@ -468,21 +557,24 @@ def run_ours(args, cfg, rank, world, local_rank):
                  "on the GPU, bf16, a distinct input per step" if args.data == "waterfall" else
                  "synthetic (seeded torch Philox; K/V ~ N(0,1), q ~ N(0, 2.5^2), bf16)"),
         "config": {"workload": cfg["workload"], "model_shapes": cfg["model"], "layers": nl,
-                   "per_gpu_batch": B, "global_batch": B if heads else B * world, "prefill": P, "L": L,
+                   "unit_detail": unit_detail(B_global if mode == "strong" else B, nl, world, mode),
+                   "per_gpu_batch": B, "global_batch": B_global if not heads else B,
+                   "prefill": P, "L": L,
                    "page": args.page, "alpha": args.alpha, "score_mode": args.score,
                    "stamp_rule": f"top-r {args.top_r}" if args.top_r > 0 else "alpha",
                    "quest_prefill_pages": args.quest_prefill,
                    "table_scope": "request" if args.table_scope else "kv-head",
                    "variant": variant_name(args),
-                   "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per layer-step"
-                                   if heads else f"request-sharded x{world}, no collective"),
-                   "l2": (f"{nl} distinct layer caches = {cache_bytes / 2**30:.2f} GiB "
-                          + ("> 126 MB L2 (no flush needed)" if cache_bytes > 126e6 else
-                             "< 126 MB L2: part of the K/V stream can hit in L2")),
+                   "parallelism": (f"head-sharded x{world}: kv-heads split, NCCL all-gather of out per "
+                                   f"layer-step{' (in the CUDA graph)' if graphed else ' (eager, gloo)'}"
+                                   if heads else
+                                   f"request-sharded x{world} ({mode} scaling), no collective"),
+                   "l2": l2_note,
                    "steady_state": f"{fill_steps} decode steps before warmup (all pages used, evicting)"},
-        "tokens_per_s": value * B,
+        "tokens_per_s": tokens_per_s,
         "achieved_note": ("per-GPU HBM figures; the roofline covers this rank's decode launches"
                           if world > 1 else None),
+        "per_rank_ms": per_rank,
         "layer_steps_per_s": value * nl,
         "hbm_gbs": achieved,
         "pct_of_8tbs": achieved / 8000.0 * 100.0,
@@ -498,7 +590,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "timing": "CUDA events on the launch stream around K graph replays of "
                                f"{nl} launches; avg launch = step / {nl}"},
         "e2e": e2e,
-        "gpu_launches": args.steps * nl * (2 if args.quest_prefill else 1),
+        "gpu_launches": args.steps * nl * (2 if args.quest_prefill else 1) * world,
         "launch": info,
         "stamp_rate": stamps / max(decisions, 1),
         "evictions_per_step": evictions / max(unit_steps, 1) * units,
@@ -510,32 +602,48 @@ def run_ours(args, cfg, rank, world, local_rank):
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the CPU oracle (as it stands) on a bounded sample, same metric."""
-    if rank != 0:
-        return None
-    units = cfg["batch"] * cfg["hkv"]
-    ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
-    v = ups / (units * cfg["layers"])
-    return {
-        "impl": "reference",
-        "metric": METRIC,
-        "value": v,
-        "unit": "decode steps/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": cfg["workload"], "per_gpu_batch": cfg["batch"], "L": cfg["L"],
-                   "layers": cfg["layers"]},
-        "cpu_baseline": {"value": v, "unit": "decode steps/s", "cores": threads, "kind": "oracle",
-                         "sample": desc},
-        "e2e": {"value": v, "unit": "decode steps/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
+    """--impl reference: the CPU oracle (as it stands) on a bounded sample, same metric, unit and
+    config as our arm.  Under N ranks, rank 0 alone works and prints; the others join the
+    process group (gloo, CPU), wait at the barriers and exit 0."""
+    import torch
+
+    if world > 1:
+        torch.distributed.init_process_group("gloo")
+        torch.distributed.barrier()
+    out = None
+    if rank == 0:
+        units = cfg["batch"] * cfg["hkv"]
+        t0 = time.perf_counter()
+        ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
+        wall = time.perf_counter() - t0
+        v = ups / (units * cfg["layers"])
+        out = {
+            "impl": "reference",
+            "metric": METRIC,
+            "value": v,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (full-cache state, seeded Philox, bf16 values; the oracle's bounded sample)",
+            "config": {"workload": cfg["workload"], "model_shapes": cfg["model"],
+                       "unit_detail": unit_detail(cfg["batch"], cfg["layers"], 1, "weak"),
+                       "per_gpu_batch": cfg["batch"], "L": cfg["L"], "prefill": cfg["P"],
+                       "layers": cfg["layers"],
+                       "parallelism": "rank 0 only (the oracle on the host cores)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall,
+        }
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return out
 
 
 def main():
@@ -547,7 +655,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--alpha", type=float, default=1e-4)
     ap.add_argument("--L", type=int, default=0, help="override the budget (config 5 sweep)")
-    ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch")
+    ap.add_argument("--batch", type=int, default=0, help="override the per-GPU (weak) / global (strong) batch")
     ap.add_argument("--layers", type=int, default=0, help="override the layer count")
     ap.add_argument("--fill", type=int, default=-1, help="decode steps before warmup (-1: auto)")
     ap.add_argument("--data", default="waterfall", choices=["waterfall", "gaussian"],
@@ -558,7 +666,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
-                    help="multi-GPU: shard requests (weak scaling) or kv-heads (strong, all-gather)")
+                    help="multi-GPU: shard requests (no collective) or kv-heads (all-gather of out)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="request sharding: fixed per-GPU batch (weak) or fixed global batch (strong)")
+    ap.add_argument("--rotate", type=int, default=-1,
+                    help="layer-cache rotations (-1: enough for >= 4x L2 of distinct caches)")
     ap.add_argument("--split-pages", type=int, default=0, help="override pages per split tile")
     ap.add_argument("--quest-prefill", type=int, default=0,
                     help="Quest-on-prefill hybrid: prompt pages attended per step (NEXT-4)")
@@ -574,6 +686,13 @@ def main():
     ap.add_argument("--dense", type=int, default=0,
                     help="dense comparator: prefill N tokens, L > N + steps (no eviction)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     cfg = dict(CONFIGS[args.config])
     if args.L:
         cfg["L"] = args.L
@@ -585,16 +704,16 @@ def main():
         args.fill = 0
     if args.batch:
         cfg["batch"] = args.batch
+        cfg["global_batch"] = args.batch
     if args.P:
         cfg["P"] = args.P
         cfg["workload"] += f"_P{args.P}"
     if args.layers:
         cfg["layers"] = args.layers
+    if args.scaling == "strong" and args.shard == "requests":
+        cfg["workload"] = cfg["workload"].replace("_b32pergpu", "") + f"_strong_b{cfg.get('global_batch', cfg['batch'])}"
     args.warmup = max(args.warmup, 3)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     # RAAS_BENCH_SHARE_GPU=1: test mode for the multi-rank path on a single GPU (ranks share
     # device 0, gloo carries the barriers and the timing reduction); never a bench number
     share = os.environ.get("RAAS_BENCH_SHARE_GPU") == "1"

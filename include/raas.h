@@ -93,8 +93,8 @@ typedef struct {
                             other resident pages; stamping / eviction are unchanged (prompt pages
                             stay pinned and resident).  Adds one small launch per step
                             (bound + selection) and 1/16 of the prompt's K bytes.  L <= 8192.
-                            With raas_set_state, every pinned page is treated as a full prompt
-                            page. */
+                            With raas_set_state, the selectable pages are the pinned pages
+                            flagged 1 (a flag-2 partial last prompt page is always attended). */
   int32_t table_scope;   /* page-table granularity (reading D25):
                             0 = one table per (request, kv-head), stamped when any q-head of the
                                 GQA group exceeds the threshold (reading D5, default);
@@ -104,6 +104,8 @@ typedef struct {
                                 arrays keep one identical replica per kv-head; raas_set_state
                                 rejects replicas that differ.  Sharding a request's kv-heads over
                                 handles would need an exchange, so shard by request only. */
+  int32_t disable_early_start; /* 0 (default) = early start allowed, 1 = never (see "Early start"
+                            below); changes timing only, never results */
 } raas_config;
 
 /* Bytes of device memory the handle needs (KV store: per unit L/16 pages, each 16 K rows + 16 V
@@ -130,6 +132,26 @@ RAAS_API int raas_prefill(raas_handle* h, const void* k, const void* v, int32_t 
  * raas_prefill(h, k, v, P, s) is raas_prefill_varlen with every P_host[b] = P_max = P. */
 RAAS_API int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int32_t* P_host,
                                  int32_t P_max, void* stream);
+
+/* Early start (programmatic dependent launch, PDL).  raas_decode_step launches with the
+ * programmatic-stream-serialization attribute and calls griddepcontrol.launch_dependents right
+ * after its own griddepcontrol.wait.  When the kernel right before it in the stream is NOT this
+ * handle's previous decode step (the usual case: one handle per layer, layers interleaved on one
+ * stream), the kernel reads its handle's state (write plan, page counts) and issues its first
+ * K/V page copies BEFORE griddepcontrol.wait, overlapping the previous kernel's tail.  This is
+ * safe because the handle's previous step then completed before the previous kernel could
+ * trigger this one.  CONTRACT for callers that enable it (the default):
+ *   - every PDL kernel placed on the same stream between two steps of one handle must trigger
+ *     its dependents only after its own griddepcontrol.wait (standard practice; a kernel that
+ *     triggers earlier could let a decode step read state its own previous step is still
+ *     writing);
+ *   - nothing but libraas may write a handle's arena between its steps (raas_set_state and
+ *     raas_prefill are stream-ordered and reset the tracking).
+ * The library tracks, per stream, the last handle it launched a decode step for; a handle
+ * stepped twice in a row waits as usual.  Set cfg.disable_early_start = 1 to never read state
+ * before griddepcontrol.wait (e.g. when foreign PDL kernels that trigger early share the
+ * stream).  The Quest-on-prefill hybrid never starts early (its selection kernel, launched right
+ * before the step, writes the attended-page list). */
 
 /* One decode step for every unit of the handle:
  *   t += 1; pick the slot (current page, else a fresh page, else the victim chosen at the end
@@ -158,16 +180,20 @@ RAAS_API int raas_destroy(raas_handle* h);
 /* ---- introspection / test support (synchronise `stream`) ---- */
 
 /* Host copies of the page metadata: t[units] (tokens so far), ts/start_pos/count [units][L/16]
- * int32, pinned [units][L/16] uint8.  Pinned pages report ts = 0 (D17).  Any output may be
- * NULL. */
+ * int32, pinned [units][L/16] uint8: 0 = unpinned, 1 = a prompt page that was full at prefill,
+ * 2 = the prompt's partial last page (P % 16 != 0: decode tokens fill it and it stays pinned,
+ * reading D13; the Quest-on-prefill hybrid never drops it, D24).  Pinned pages report ts = 0
+ * (D17).  Any output may be NULL. */
 RAAS_API int raas_get_state(raas_handle* h, int32_t* t, int32_t* ts, int32_t* start_pos, int32_t* count,
                    uint8_t* pinned, void* stream);
 
 /* Lockstep resync (SURVEY.md §8c parity protocol): overwrite the metadata (host arrays in the
- * raas_get_state layout; pinned pages must be a prefix 0..Pp-1 of each unit, decode pages must
- * be the pages that follow) and, if non-NULL, the KV store from host bf16 arrays
- * [units][L/16][16][head_dim].  The write cursor and the next victim are re-derived on the
- * device.  Marks the handle prefilled. */
+ * raas_get_state layout; pinned pages must be a prefix 0..Pp-1 of each unit, only the last of
+ * them may carry flag 2, decode pages must be the pages that follow) and, if non-NULL, the KV
+ * store from host bf16 arrays [units][L/16][16][head_dim].  The write cursor (the used page
+ * with the largest start position) and the next victim are re-derived on the device, so
+ * get_state -> set_state continues bitwise as the uninterrupted run.  Marks the handle
+ * prefilled.  RAAS_E_INVALID on a malformed state (nothing is written). */
 RAAS_API int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const int32_t* start_pos,
                    const int32_t* count, const uint8_t* pinned, const void* k_store_host,
                    const void* v_store_host, void* stream);

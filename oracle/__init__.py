@@ -73,6 +73,7 @@ def lib():
         l.raas_ref_get_state.argtypes = [P, P, P, P, P, P]
         l.raas_ref_set_state.argtypes = [P, P, P, P, P, P, P, P]
         l.raas_ref_get_trace.argtypes = [P, P, P, P]
+        l.raas_ref_get_kv.argtypes = [P, P, P]
         l.raas_ref_resident_positions.argtypes = [P, ctypes.c_int32, P, ctypes.c_int32]
         l.raas_ref_get_selection.argtypes = [P, P, P]
         l.raas_ref_set_threads.argtypes = [ctypes.c_int]
@@ -174,6 +175,15 @@ class Oracle:
         rc = lib().raas_ref_set_state(self._h, *[_ptr(x) for x in a], _ptr(pin), _ptr(ks), _ptr(vs))
         if rc:
             raise OracleError(rc, "raas_ref_set_state")
+
+    def get_kv(self):
+        """K and V stores as bf16 bits [units][C][page][head_dim]."""
+        shape = (self.units, self.C, self.page, self.d)
+        ks, vs = np.zeros(shape, np.uint16), np.zeros(shape, np.uint16)
+        rc = lib().raas_ref_get_kv(self._h, _ptr(ks), _ptr(vs))
+        if rc:
+            raise OracleError(rc, "raas_ref_get_kv")
+        return ks, vs
 
     def get_trace(self):
         U, C = self.units, self.C

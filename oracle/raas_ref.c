@@ -423,8 +423,31 @@ int raas_ref_get_state(const raas_ref* h, int32_t* t, int32_t* ts, int32_t* star
     if (ts) memcpy(ts + (size_t)ui * C, u->ts, (size_t)C * sizeof(int32_t));
     if (start_pos) memcpy(start_pos + (size_t)ui * C, u->start, (size_t)C * sizeof(int32_t));
     if (count) memcpy(count + (size_t)ui * C, u->count, (size_t)C * sizeof(int32_t));
-    if (pinned) memcpy(pinned + (size_t)ui * C, u->pinned, (size_t)C);
+    /* pinned flags: 1 = a prompt page that was full at prefill (selectable by the hybrid, D24),
+     * 2 = the prompt's partial last page (P % page != 0; decode tokens fill it, D13) */
+    if (pinned)
+      for (int32_t p = 0; p < C; ++p)
+        pinned[(size_t)ui * C + p] = u->pinned[p] ? (p < u->nfull ? 1 : 2) : 0;
   }
+  return REF_OK;
+}
+
+/* bf16 bits of a double that holds an exact bf16 value (every stored K/V element does) */
+static uint16_t narrow_bf16(double x) {
+  const float f = (float)x;
+  uint32_t b;
+  memcpy(&b, &f, sizeof b);
+  return (uint16_t)(b >> 16);
+}
+
+int raas_ref_get_kv(const raas_ref* h, uint16_t* k_store, uint16_t* v_store) {
+  if (!h) return REF_E_INVALID;
+  const size_t kv = (size_t)h->C * h->cfg.page * h->cfg.head_dim;
+  for (int32_t ui = 0; ui < h->units; ++ui)
+    for (size_t i = 0; i < kv; ++i) {
+      if (k_store) k_store[(size_t)ui * kv + i] = narrow_bf16(h->u[ui].K[i]);
+      if (v_store) v_store[(size_t)ui * kv + i] = narrow_bf16(h->u[ui].V[i]);
+    }
   return REF_OK;
 }
 
@@ -440,12 +463,13 @@ int raas_ref_set_state(raas_ref* h, const int32_t* t, const int32_t* ts,
     memcpy(u->ts, ts + (size_t)ui * C, (size_t)C * sizeof(int32_t));
     memcpy(u->start, start_pos + (size_t)ui * C, (size_t)C * sizeof(int32_t));
     memcpy(u->count, count + (size_t)ui * C, (size_t)C * sizeof(int32_t));
-    memcpy(u->pinned, pinned + (size_t)ui * C, (size_t)C);
+    u->nfull = 0;
+    for (int32_t p = 0; p < C; ++p) {
+      u->pinned[p] = pinned[(size_t)ui * C + p] != 0;
+      if (pinned[(size_t)ui * C + p] == 1) u->nfull += 1;  /* flag 1: full prompt page (D24) */
+    }
     u->used = 0;
     u->cur = -1;
-    u->nfull = 0;
-    for (int32_t p = 0; p < C; ++p)
-      if (u->pinned[p]) u->nfull += 1;            /* set_state: pinned pages are full prompt pages */
     for (int32_t p = 0; p < C; ++p) {
       if (u->count[p] > 0) {
         u->used += 1;

@@ -78,15 +78,21 @@ int  raas_ref_decode_step(raas_ref* h, const uint16_t* q, const uint16_t* k_new,
  * or empty pages).  No K/V data is written or attended. */
 int  raas_ref_step_stamps(raas_ref* h, const uint8_t* stamps);
 
-/* state readout; any pointer may be NULL.  t[unit] = tokens so far (PAPER.md :394). */
+/* state readout; any pointer may be NULL.  t[unit] = tokens so far (PAPER.md :394).
+ * pinned[unit*C+p]: 0 = unpinned; 1 = prompt page full at prefill; 2 = the prompt's partial
+ * last page (P % page != 0), which decode tokens fill (D13) and the hybrid never selects (D24). */
 int  raas_ref_get_state(const raas_ref* h, int32_t* t, int32_t* ts, int32_t* start_pos,
                         int32_t* count, uint8_t* pinned);
 /* lockstep resync (SURVEY §8c parity protocol): overwrite metadata and, when non-NULL,
- * the KV store (bf16 bits, [units][C][page][head_dim]).  cur/used are re-derived. */
+ * the KV store (bf16 bits, [units][C][page][head_dim]).  cur/used are re-derived; the
+ * hybrid's full prompt pages are the pages flagged 1 (see raas_ref_get_state). */
 int  raas_ref_set_state(raas_ref* h, const int32_t* t, const int32_t* ts,
                         const int32_t* start_pos, const int32_t* count,
                         const uint8_t* pinned, const uint16_t* k_store,
                         const uint16_t* v_store);
+/* KV store readout (bf16 bits, [units][C][page][head_dim]; never-written rows are 0);
+ * either pointer may be NULL.  With raas_ref_get_state it is the whole resync state. */
+int  raas_ref_get_kv(const raas_ref* h, uint16_t* k_store, uint16_t* v_store);
 /* trace of the LAST step:
  *   evicted[unit]  = start_pos of the page evicted before attention, or -1
  *   slot[unit]     = page index the new token was written to

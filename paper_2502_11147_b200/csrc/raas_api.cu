@@ -106,6 +106,8 @@ int derive(const raas_config* c, Derived* d) {
     return fail(RAAS_E_UNSUPPORTED, "top-r stamping supports at most 512 pages (token slots) per unit");
   if (c->quest_prefill_pages < 0) return fail(RAAS_E_INVALID, "quest_prefill_pages must be >= 0");
   if (c->table_scope != 0 && c->table_scope != 1) return fail(RAAS_E_INVALID, "table_scope must be 0 or 1");
+  if (c->disable_early_start != 0 && c->disable_early_start != 1)
+    return fail(RAAS_E_INVALID, "disable_early_start must be 0 or 1");
   if (c->quest_prefill_pages > 0 && d->C > 512)
     return fail(RAAS_E_UNSUPPORTED, "the Quest-on-prefill hybrid supports L <= 8192 (512 pages)");
   d->units = c->batch * c->n_kv_heads;
@@ -293,10 +295,10 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
     // after_copies: staged cudaMemcpyAsync copies precede this launch (full serialisation).
     // The zero-copy ingest kernel triggers us at its start, so it does not count: the kernel
     // two back has completed, the one right before (this handle's or not) may still run.
-    static const bool no_early = std::getenv("RAAS_NO_EARLY") != nullptr;  // A/B experiments
     // not with the Quest-on-prefill hybrid: its selection kernel (this handle's) runs right
-    // before the decode kernel and writes the attended-page list the producer reads
-    p.early = (other || after_copies) && h->cfg.quest_prefill_pages == 0 && !no_early;
+    // before the decode kernel and writes the attended-page list the producer reads; not when
+    // the caller opted out (raas.h "Early start")
+    p.early = (other || after_copies) && h->cfg.quest_prefill_pages == 0 && !h->cfg.disable_early_start;
   }
   p.n_kv = h->cfg.n_kv_heads;
   p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;
@@ -653,10 +655,11 @@ int raas_get_state(raas_handle* h, int32_t* t, int32_t* ts, int32_t* start_pos, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t U = h->d.units, C = h->d.Ce;  // metadata entries (pages, or token slots)
   if (int rc = tok_flush(h, st)) return rc;
-  std::vector<int32_t> npin(U), vts(U * C);
+  std::vector<int32_t> npin(U), nfull(U), vts(U * C);
   std::vector<int4> plan(U);
   uint8_t* a = h->arena;
   RAAS_CUDA(cudaMemcpyAsync(npin.data(), a + h->lay.npin, U * 4, cudaMemcpyDeviceToHost, st));
+  RAAS_CUDA(cudaMemcpyAsync(nfull.data(), a + h->lay.nfull, U * 4, cudaMemcpyDeviceToHost, st));
   RAAS_CUDA(cudaMemcpyAsync(plan.data(), a + h->lay.plan, U * 16, cudaMemcpyDeviceToHost, st));
   RAAS_CUDA(cudaMemcpyAsync(vts.data(), a + h->lay.ts, U * C * 4, cudaMemcpyDeviceToHost, st));
   if (start_pos)
@@ -669,7 +672,8 @@ int raas_get_state(raas_handle* h, int32_t* t, int32_t* ts, int32_t* start_pos, 
     for (size_t p = 0; p < C; ++p) {
       const bool pin = (int)p < npin[u];
       if (ts) ts[u * C + p] = pin ? 0 : vts[u * C + p];
-      if (pinned) pinned[u * C + p] = pin ? 1 : 0;
+      // 1 = prompt page full at prefill, 2 = the prompt's partial last page (D13 / D24)
+      if (pinned) pinned[u * C + p] = pin ? ((int)p < nfull[u] ? 1 : 2) : 0;
     }
   }
   return RAAS_OK;
@@ -683,13 +687,19 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   DeviceGuard guard(h->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t U = h->d.units, C = h->d.Ce;  // metadata entries (pages, or token slots)
-  std::vector<int32_t> npin(U);
+  std::vector<int32_t> npin(U), nfull(U);
   std::vector<int4> plan(U);
   for (size_t u = 0; u < U; ++u) {
     int np = 0;
     while (np < (int)C && pinned[u * C + np]) ++np;
     for (size_t p = np; p < C; ++p)
       if (pinned[u * C + p]) return fail(RAAS_E_INVALID, "pinned pages must be a prefix (unit %zu)", u);
+    // flag 2 marks the prompt's partial last page: only the last pinned page may carry it
+    for (int p = 0; p + 1 < np; ++p)
+      if (pinned[u * C + p] != 1)
+        return fail(RAAS_E_INVALID, "pinned flag 2 (partial prompt page) on a page that is not the last pinned one (unit %zu)", u);
+    if (np > 0 && pinned[u * C + np - 1] > 2) return fail(RAAS_E_INVALID, "pinned flag > 2 (unit %zu)", u);
+    nfull[u] = (np > 0 && pinned[u * C + np - 1] == 2) ? np - 1 : np;
     bool hole = false;
     for (size_t p = 0; p < C; ++p) {
       if (count[u * C + p] < 0 || count[u * C + p] > h->d.ep)
@@ -717,8 +727,8 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.start, start_pos, U * C * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.cnt, count, U * C * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.npin, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
-  // set_state: the pinned pages are taken as full prompt pages (hybrid selection set)
-  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.nfull, npin.data(), U * 4, cudaMemcpyHostToDevice, st));
+  // the hybrid's selectable prompt pages: the pinned pages flagged 1 (D24)
+  RAAS_CUDA(cudaMemcpyAsync(a + h->lay.nfull, nfull.data(), U * 4, cudaMemcpyHostToDevice, st));
   RAAS_CUDA(cudaMemcpyAsync(a + h->lay.plan, plan.data(), U * 16, cudaMemcpyHostToDevice, st));
   const size_t pages = U * h->d.C, D = h->cfg.head_dim;  // 16-row tiles
   std::vector<uint16_t> dev;

@@ -39,6 +39,7 @@ class raas_config(ctypes.Structure):
         ("top_r", ctypes.c_float),
         ("quest_prefill_pages", ctypes.c_int32),
         ("table_scope", ctypes.c_int32),
+        ("disable_early_start", ctypes.c_int32),
     ]
 
 
@@ -104,9 +105,11 @@ STAMP_ALPHA, STAMP_TOP_R = 0, 1
 
 def make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch, page=16, softmax_scale=0.0,
                 split_pages=0, score_mode=SCORE_EXACT, stamp_rule=STAMP_ALPHA,
-                top_r=0.5, quest_prefill_pages=0, table_scope=0) -> raas_config:
+                top_r=0.5, quest_prefill_pages=0, table_scope=0,
+                disable_early_start=0) -> raas_config:
     return raas_config(L, alpha, page, n_q_heads, n_kv_heads, head_dim, batch, softmax_scale,
-                       split_pages, score_mode, stamp_rule, top_r, quest_prefill_pages, table_scope)
+                       split_pages, score_mode, stamp_rule, top_r, quest_prefill_pages, table_scope,
+                       disable_early_start)
 
 
 def raas_arena_bytes(cfg: raas_config) -> int:
@@ -139,13 +142,14 @@ class RaasLayer:
     def __init__(self, L, alpha, n_q_heads, n_kv_heads, head_dim, batch, device=None,
                  softmax_scale=0.0, split_pages=0, score_mode=SCORE_EXACT,
                  stamp_rule=STAMP_ALPHA, top_r=0.5, quest_prefill_pages=0, table_scope=0,
-                 page=16):
+                 page=16, disable_early_start=0):
         import torch
 
         self.cfg = make_config(L, alpha, n_q_heads, n_kv_heads, head_dim, batch, page=page,
                                softmax_scale=softmax_scale, split_pages=split_pages,
                                score_mode=score_mode, stamp_rule=stamp_rule, top_r=top_r,
-                               quest_prefill_pages=quest_prefill_pages, table_scope=table_scope)
+                               quest_prefill_pages=quest_prefill_pages, table_scope=table_scope,
+                               disable_early_start=disable_early_start)
         self.device = torch.device(device if device is not None else "cuda")
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         nbytes = raas_arena_bytes(self.cfg)

@@ -6,7 +6,9 @@ Units (request, kv-head) are independent (reading D5), so the path shards with n
   own handles and arenas; NCCL is used only for barriers and the max-over-ranks timing.
 * head sharding (for small batches, e.g. config 2 at B = 1): rank r owns a contiguous block of
   kv-heads and their q-heads; the step is the same kernel over this rank's units, followed by
-  one all-gather of `out` per layer-step (the only collective of the path).
+  one all-gather of `out` per layer-step (the only collective of the path).  ``HeadGather``
+  preallocates its buffers, so the decode launches and the NCCL all-gathers of a model step
+  are captured together in one CUDA graph.
 
 The helpers here are plain index arithmetic and torch.distributed calls; the decode itself is
 always libraas on this rank's GPU.
@@ -68,3 +70,39 @@ def gather_heads(out_local, out_full=None):
         out_full.copy_(full)
         return out_full
     return full
+
+
+class HeadGather:
+    """Preallocated all-gather of a head-sharded output, [B, Hq/G, d] per rank -> [B, Hq, d]
+    (rank r's heads at [r*Hq/G, (r+1)*Hq/G)).  Nothing is allocated per call, so a step that
+    uses it can be captured in a CUDA graph with NCCL (all_gather_into_tensor is capturable).
+    At B = 1 the rank-major gather layout [G][1][Hq/G][d] IS [1][Hq][d]: NCCL writes the final
+    tensor directly; for B > 1 one strided copy reorders it.  gloo (CPU tests, the bench's
+    shared-GPU test mode) goes through the host and is not capturable."""
+
+    def __init__(self, B, hq_local, d, dtype, device):
+        import torch
+        import torch.distributed as dist
+
+        self.world = dist.get_world_size()
+        self.B, self.hl, self.d = B, hq_local, d
+        self.nccl = dist.get_backend() == "nccl"
+        self.full = torch.empty((B, self.world * hq_local, d), dtype=dtype, device=device)
+        self.stacked = (self.full if B == 1 else
+                        torch.empty((self.world, B, hq_local, d), dtype=dtype, device=device))
+        self.capturable = self.nccl
+
+    def __call__(self, out_local):
+        import torch
+        import torch.distributed as dist
+
+        if self.nccl:
+            dist.all_gather_into_tensor(self.stacked, out_local)
+        else:
+            loc = out_local.contiguous().cpu()
+            parts = [torch.empty_like(loc) for _ in range(self.world)]
+            dist.all_gather(parts, loc)
+            self.stacked.copy_(torch.stack(parts).view(self.stacked.shape))
+        if self.B > 1:
+            self.full.view(self.B, self.world, self.hl, self.d).copy_(self.stacked.permute(1, 0, 2, 3))
+        return self.full

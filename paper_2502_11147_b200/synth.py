@@ -236,3 +236,93 @@ class WaterfallTorch:
         k_out.view(U, d).copy_(self.phi[:, cur] + self.key_noise * z / math.sqrt(d))
         v_out.view(U, d).copy_(torch.randn((U, d), device=self.dev, generator=self.gen))
         self.i += 1
+
+
+def waterfall_resume(seed, B, Hq, Hkv, d, L, P, T, cur_count=5, lam=6.0, eta=1.0, key_noise=0.5,
+                     p_milestone=0.1, milestone_half_life=256.0, p_phoenix=1.0 / 512,
+                     phoenix_len=32, recent_weight=0.8, phoenix_weight=0.8, span=4):
+    """A full-cache state in the middle of a long waterfall decode, plus the next T steps.
+
+    For the full-size parity runs (configs 2-5), which cannot afford the oracle over the whole
+    fill: every unit holds its prompt pages (pinned) and C - Pp decode pages of logical pages of
+    the waterfall workload (``waterfall_stream``'s recipe: page signatures phi, keys
+    phi + key_noise z / sqrt(d), queries lam sqrt(d) sum_p w_p(t) phi_p + eta zeta with the sink,
+    the two most recent pages, decaying milestones and phoenix prompt pages).  The write page is
+    the current logical page m_cur holding ``cur_count`` tokens (1..16; < 16: a partial current
+    page), so t_now = 16 m_cur + cur_count.  The other resident decode pages are drawn among the
+    ``span`` * (C - Pp) logical pages before m_cur, the milestone pages preferred (what a
+    retention policy keeps), in random slots; their timestamps are drawn in [last position,
+    t_now].  Draws numbers only: no attention, stamping or eviction rule is applied.
+
+    Returns (state dict(t, ts, start, count, pinned) [units][C], k_store, v_store bf16 bits
+    [units][C][16][d], Stream with k_pre/v_pre = None and T steps of q / k / v)."""
+    assert P % PAGE == 0, "prompt pages are full here"
+    assert 1 <= cur_count <= PAGE
+    rng = np.random.Generator(np.random.Philox(seed))
+    g, U = Hq // Hkv, B * Hkv
+    C, Pp = L // PAGE, P // PAGE
+    nd = C - Pp
+    assert nd >= 2
+    m_cur = Pp + span * nd                                   # logical page of token t_now
+    t_now = PAGE * m_cur + cur_count
+    n_pages = m_cur + (cur_count + T) // PAGE + 2
+    phi = rng.standard_normal((U, n_pages, d), dtype=np.float32)
+    phi /= np.linalg.norm(phi, axis=-1, keepdims=True)
+    first_pos = np.arange(n_pages) * PAGE + 1
+    ms = (rng.random((U, n_pages)) < p_milestone) & (first_pos > P)[None, :]
+    ms_strength = (rng.uniform(0.2, 1.0, (U, n_pages)) * ms).astype(np.float32)
+    # resident logical pages per unit: prompt 0..Pp-1, m_cur, and nd - 1 of [m_cur - span*nd, m_cur)
+    cand = np.arange(m_cur - span * nd, m_cur)
+    logical = np.zeros((U, C), np.int64)
+    logical[:, :Pp] = np.arange(Pp)
+    pick_score = ms_strength[:, cand] + 0.05 * rng.random((U, len(cand)))
+    older = cand[np.argsort(-pick_score, axis=1, kind="stable")[:, : nd - 1]]
+    dec = np.concatenate([older, np.full((U, 1), m_cur)], axis=1)
+    perm = rng.permuted(np.tile(np.arange(nd), (U, 1)), axis=1)       # random physical slots
+    logical[:, Pp:] = np.take_along_axis(dec, perm, axis=1)
+    start = (PAGE * logical + 1).astype(np.int32)
+    count = np.full((U, C), PAGE, np.int32)
+    count[logical == m_cur] = cur_count
+    pinned = np.zeros((U, C), np.uint8)
+    pinned[:, :Pp] = 1
+    last = start + count - 1
+    ts = np.minimum(t_now, last + rng.integers(0, 8 * PAGE, (U, C))).astype(np.int32)
+    ts[logical == m_cur] = t_now
+    ts[:, :Pp] = 0
+    state = dict(t=np.full(U, t_now, np.int32), ts=ts, start=start, count=count, pinned=pinned)
+    # the stores: row i of a resident page holds position start + i (rows >= count are unused)
+    k_st = np.empty((U, C, PAGE, d), np.uint16)
+    v_st = np.empty((U, C, PAGE, d), np.uint16)
+    for u in range(U):
+        z = rng.standard_normal((C, PAGE, d), dtype=np.float32)
+        k_st[u] = bf16_bits(phi[u, logical[u]][:, None, :] + key_noise * z / np.sqrt(d))
+        v_st[u] = bf16_bits(rng.standard_normal((C, PAGE, d), dtype=np.float32))
+    # the next T steps (new token at position t = t_now + 1 + i)
+    pp = Pp
+    phoenix_until = np.full(U, -1, np.int64)
+    phoenix_page = np.zeros(U, np.int64)
+    q = np.empty((T, B, Hq, d), np.float32)
+    kn = np.empty((T, B, Hkv, d), np.float32)
+    for i in range(T):
+        t = t_now + 1 + i
+        cur = (t - 1) // PAGE
+        lo = max(0, cur - int(16 * milestone_half_life / PAGE))      # older milestones: < 2^-16
+        age = t - first_pos[lo: cur + 1]
+        w = ms_strength[:, lo: cur + 1] * (2.0 ** (-np.maximum(age, 0) / milestone_half_life))[None, :]
+        w[:, cur - lo] = np.maximum(w[:, cur - lo], recent_weight)
+        w[:, cur - 1 - lo] = np.maximum(w[:, cur - 1 - lo], recent_weight)
+        start_ph = (rng.random(U) < p_phoenix) & (phoenix_until < t)
+        phoenix_page[start_ph] = rng.integers(0, pp, int(start_ph.sum()))
+        phoenix_until[start_ph] = t + phoenix_len
+        base = np.einsum("up,upd->ud", w, phi[:, lo: cur + 1])
+        base += phi[:, 0]                                             # sink ("lazy" maps)
+        act = (phoenix_until >= t) & (phoenix_page != 0)              # page 0 is the sink already
+        base[act] += phoenix_weight * phi[act, phoenix_page[act]]
+        base *= lam * np.sqrt(d)
+        noise = eta * rng.standard_normal((U, g, d), dtype=np.float32)
+        q[i] = (base[:, None, :] + noise).reshape(B, Hq, d)
+        kn[i] = (phi[:, cur] + key_noise * rng.standard_normal((U, d), dtype=np.float32) / np.sqrt(d)
+                 ).reshape(B, Hkv, d)
+    vn = rng.standard_normal((T, B, Hkv, d), dtype=np.float32)
+    steps = Stream(None, None, bf16_bits(q), bf16_bits(kn), bf16_bits(vn))
+    return state, k_st, v_st, steps

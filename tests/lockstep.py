@@ -75,6 +75,29 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None, histo
         layer.raas_set_state(o["t"], o["ts"], o["start"], o["count"], o["pinned"])
 
 
+def compare_sampled(layer, orc, units, alpha, pstar, res):
+    """Full-size lockstep on sampled units: the oracle holds only `units` of the GPU handle.
+    Their state must be bit-exact (a differing timestamp only inside the band, counted, then
+    the GPU rows are resynced to the oracle's)."""
+    gs = layer.raas_get_state()
+    os_ = orc.get_state()
+    g = {k: v[units] for k, v in gs.items()}
+    same = all(np.array_equal(g[k], os_[k]) for k in os_)
+    if same:
+        return
+    for k in ("t", "start", "count", "pinned"):
+        assert np.array_equal(g[k], os_[k]), f"state field {k} differs outside the stamp band"
+    for u, p in np.argwhere(g["ts"] != os_["ts"]):
+        ps = pstar[u, p]
+        assert ps >= 0 and abs(ps - alpha) < BAND, (
+            f"ts differs at sampled unit {units[u]} page {p}: gpu {g['ts'][u, p]} oracle "
+            f"{os_['ts'][u, p]}, p*={ps!r} outside the |p*-alpha|<{BAND} band")
+        res.band_events += 1
+    full = {k: v.copy() for k, v in gs.items()}
+    full["ts"][units] = os_["ts"]
+    layer.raas_set_state(full["t"], full["ts"], full["start"], full["count"], full["pinned"])
+
+
 def run_lockstep(oracle_mod, stream, L, alpha, Hq, Hkv, split_pages=0, check_every=1,
                  layer=None, oracle=None, device="cuda", on_step=None, score_mode=0,
                  stamp_rule=0, top_r=0.5, quest_prefill_pages=0, table_scope=0, page=16,

@@ -16,10 +16,10 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from lockstep import OUT_TOL, from_dev, run_lockstep, to_dev  # noqa: E402
+from lockstep import OUT_TOL, LockstepResult, compare_sampled, from_dev, run_lockstep, to_dev  # noqa: E402
 from paper_2502_11147_b200.raas import RAAS_E_BUDGET, RAAS_E_STATE, RaasError, RaasLayer  # noqa: E402
 from paper_2502_11147_b200.synth import (bf16_bits, bf16_to_f32, gaussian_stream,  # noqa: E402
-                                         random_steady_state, waterfall_stream)
+                                         random_steady_state, waterfall_resume, waterfall_stream)
 from traces import page_twin_stream  # noqa: E402
 
 PAGE = 16
@@ -161,6 +161,25 @@ def test_bitwise_determinism_and_request_sharding():
         assert np.array_equal(np.concatenate([slo[k], shi[k]]), sa[k])
 
 
+def test_head_sharding_bitwise():
+    """Head sharding (SURVEY §8e, config 2's layout): two handles each holding half of the
+    kv-heads (and their q-heads) give outputs and states bitwise equal to the unsharded handle's
+    corresponding heads -- what each rank computes before the all-gather (units are independent,
+    the split arithmetic is schedule-free)."""
+    B, Hq, Hkv, d, P, T, L = 1, 32, 8, 128, 512, 300, 1024
+    st = waterfall_stream(61, B, Hq, Hkv, d, P, T)
+    full, s_full = _run_gpu(st, L, Hq, Hkv, split_pages=16)
+    g = Hq // Hkv
+    for lo, hi in ((0, 4), (4, 8)):
+        sub = type(st)(st.k_pre[:, lo:hi], st.v_pre[:, lo:hi], st.q[:, :, lo * g:hi * g],
+                       st.k[:, :, lo:hi], st.v[:, :, lo:hi])
+        part, s_part = _run_gpu(sub, L, hi * g - lo * g, hi - lo, split_pages=16)
+        assert np.array_equal(part, full[:, :, lo * g:hi * g])
+        for k in ("t", "ts", "start", "count", "pinned"):
+            assert np.array_equal(s_part[k], s_full[k][lo:hi])
+    assert s_full["count"].sum() > 0
+
+
 @pytest.mark.parametrize("mode", ["pinned_reused", "pinned_queued", "pageable"])
 def test_host_entry_point_matches_device_entry_point(mode):
     """raas_decode_step_host: pinned buffers take the zero-copy path (ingest kernel + out
@@ -266,62 +285,104 @@ def test_error_codes_gpu():
 # ------------------------------------------------------------------ full-size sampled parity
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,L,P,sp", [
-    (64, 32, 8, 2048, 256, 0),   # config 3 (headline)
-    (32, 28, 4, 4096, 128, 0),   # config 4 (per GPU)
-    (1, 32, 8, 1024, 512, 16),   # config 2 (B = 1, 16-page splits as benched)
-    (8, 32, 8, 8192, 128, 0),    # config 5, largest budget (16 splits per unit)
-    (16, 32, 8, 256, 128, 0),    # config 5, smallest budget (one split per unit)
+# Waterfall query strength per config, calibrated with the oracle on the sampled requests so the
+# page stamp rate lands in SURVEY §8(d)'s 30-60 % band (scripts/calibrate_resume.py)
+LAM_RESUME = {2: 7.0, 3: 7.0, 4: 7.0, "5a": 6.0, "5b": 10.0}
+STAMP_BAND = (0.30, 0.60)
+
+
+@pytest.mark.parametrize("cfg,B,Hq,Hkv,L,P,sp,cur", [
+    (3, 64, 32, 8, 2048, 256, 0, 5),      # config 3 (headline), partial current page
+    (3, 64, 32, 8, 2048, 256, 0, 16),     # config 3, full current page (next step opens one)
+    (4, 32, 28, 4, 4096, 128, 0, 11),     # config 4 (per GPU)
+    (2, 1, 32, 8, 1024, 512, 16, 5),      # config 2 (B = 1, 16-page splits as benched)
+    ("5a", 8, 32, 8, 8192, 128, 0, 9),    # config 5, largest budget (16 splits per unit)
+    ("5b", 16, 32, 8, 256, 128, 0, 3),    # config 5, smallest budget (one split per unit)
 ])
-def test_full_size_sampled_units_lockstep(oracle_mod, B, Hq, Hkv, L, P, sp):
-    """BASELINE.json configs' shapes in the launch configuration bench.py times: the whole
-    batch runs on the GPU from a full-cache state; the first and last request (all kv-heads)
-    are replayed on the oracle in lockstep with resync."""
-    d, T = 128, 24
-    C, Pp = L // PAGE, -(-P // PAGE)
-    U = B * Hkv
-    t_now = Pp * PAGE + 4 * PAGE * (C - Pp) + 5
-    meta = random_steady_state(77, U, C, Pp, t_now)
-    rng = np.random.Generator(np.random.Philox(78))
-    kst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
-    vst = bf16_bits(rng.standard_normal((U, C, PAGE, d), np.float32))
+def test_full_size_sampled_units_lockstep(oracle_mod, cfg, B, Hq, Hkv, L, P, sp, cur):
+    """BASELINE.json configs' shapes in the launch configuration bench.py times, on the paper's
+    workload: the whole batch runs on the GPU from a full-cache waterfall state (decode pages
+    of a long reasoning trace, a partial or full current page; synth.waterfall_resume) for 48
+    waterfall steps; the first and last request (all kv-heads) run on the oracle in lockstep
+    with resync.  The page stamp rate must be selective (30-60 %) and pages must be evicted, so
+    decisions near alpha and non-FIFO evictions are exercised (PAPER.md :88-94, :135)."""
+    d, T = 128, 48
+    state, kst, vst, steps = waterfall_resume(77 + L + cur, B, Hq, Hkv, d, L, P, T, cur_count=cur,
+                                              lam=LAM_RESUME[cfg])
     layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=sp)
-    layer.raas_set_state(meta["t"], meta["ts"], meta["start"], meta["count"], meta["pinned"], kst, vst)
+    layer.raas_set_state(state["t"], state["ts"], state["start"], state["count"], state["pinned"],
+                         kst, vst)
     sample = sorted({0, B - 1})
     units = [b * Hkv + h for b in sample for h in range(Hkv)]
     orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
                             batch=len(sample))
-    orc.set_state(meta["t"][units], meta["ts"][units], meta["start"][units], meta["count"][units],
-                  meta["pinned"][units], kst[units], vst[units])
-    g = Hq // Hkv
-    band = 0
-    worst = 0.0
+    # both sides start from the same synthetic state (the generator's bits, never the GPU's)
+    orc.set_state(*(state[k][units] for k in ("t", "ts", "start", "count", "pinned")),
+                  kst[units], vst[units])
+    del kst, vst
+    res = LockstepResult()
     out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
     for i in range(T):
-        # queries aimed at a few pages so stamping is selective
-        q = 2.5 * rng.standard_normal((B, Hq, d), np.float32)
-        qb, kb, vb = bf16_bits(q), bf16_bits(rng.standard_normal((B, Hkv, d), np.float32)), \
-            bf16_bits(rng.standard_normal((B, Hkv, d), np.float32))
-        layer.raas_decode_step(to_dev(qb), to_dev(kb), to_dev(vb), out)
-        o_out = orc.decode_step(qb[sample], kb[sample], vb[sample])
-        gs = layer.raas_get_state()
-        os_ = orc.get_state()
-        tr = orc.get_trace()
+        layer.raas_decode_step(to_dev(steps.q[i]), to_dev(steps.k[i]), to_dev(steps.v[i]), out)
+        o_out = orc.decode_step(steps.q[i][sample], steps.k[i][sample], steps.v[i][sample])
         g_out = bf16_to_f32(from_dev(out)).astype(np.float64)[sample]
-        worst = max(worst, np.abs(g_out - o_out).max())
-        for k in ("t", "start", "count", "pinned"):
-            assert np.array_equal(gs[k][units], os_[k])
-        diff = np.argwhere(gs["ts"][units] != os_["ts"])
-        for u, p in diff:
-            assert abs(tr["pstar"][u, p] - 1e-4) < 1e-6
-            band += 1
-        if len(diff):
-            full = {k: gs[k].copy() for k in gs}
-            for j, u in enumerate(units):
-                full["ts"][u] = os_["ts"][j]
-            layer.raas_set_state(full["t"], full["ts"], full["start"], full["count"], full["pinned"])
-    assert worst <= OUT_TOL
-    assert band == 0
+        res.max_err = max(res.max_err, float(np.abs(g_out - o_out).max()))
+        tr = orc.get_trace()
+        res.evictions += int((tr["evicted"] >= 0).sum())
+        res.stamp_decisions += int((tr["pstar"] >= 0).sum())
+        res.stamps += int((tr["pstar"] > 1e-4).sum())
+        compare_sampled(layer, orc, units, 1e-4, tr["pstar"], res)
+    rate = res.stamps / res.stamp_decisions
+    assert res.band_events == 0
+    assert res.max_err <= OUT_TOL
+    assert STAMP_BAND[0] <= rate <= STAMP_BAND[1], f"page stamp rate {rate:.3f} not selective"
+    assert res.evictions >= len(units) * (T // PAGE)
+    assert layer.raas_get_status() == 0
+
+
+def test_bench_waterfall_stream_lockstep(oracle_mod):
+    """The exact stream bench.py times at config 3 (WaterfallTorch drawn on the GPU, lambda = 7,
+    seed 1000 * 3 + rank 0): prefill, the bench's fill to steady state ((C - Pp) * 16 + 256
+    steps), then 48 more; the first and last request (all kv-heads) replayed on the oracle on
+    the GPU-drawn input bits, compared every step.  The measured stream is parity-checked."""
+    from paper_2502_11147_b200.synth import WaterfallTorch
+
+    B, Hq, Hkv, d, P, L = 64, 32, 8, 128, 256, 2048
+    C, Pp = L // PAGE, P // PAGE
+    fill = (C - Pp) * PAGE + 256
+    T = fill + 48
+    dev = torch.device("cuda")
+    wf = WaterfallTorch(1000 * 3 + 0, B, Hq, Hkv, d, P, T + 8, dev, lam=7.0)
+    k, v = wf.prefill()
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    layer.raas_prefill(k, v, P)
+    sample = [0, B - 1]
+    units = [b * Hkv + h for b in sample for h in range(Hkv)]
+    orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
+                            batch=len(sample))
+    orc.prefill(from_dev(k[sample]), from_dev(v[sample]), P)
+    del k, v
+    q = torch.empty((B, Hq, d), dtype=torch.bfloat16, device=dev)
+    kn, vn = (torch.empty((B, Hkv, d), dtype=torch.bfloat16, device=dev) for _ in range(2))
+    out = torch.empty_like(q)
+    res, tail = LockstepResult(), LockstepResult()
+    for i in range(T):
+        wf.step(q, kn, vn)
+        layer.raas_decode_step(q, kn, vn, out)
+        o_out = orc.decode_step(from_dev(q[sample]), from_dev(kn[sample]), from_dev(vn[sample]))
+        g_out = bf16_to_f32(from_dev(out)).astype(np.float64)[sample]
+        r = tail if i >= fill else res
+        r.max_err = max(r.max_err, float(np.abs(g_out - o_out).max()))
+        tr = orc.get_trace()
+        r.evictions += int((tr["evicted"] >= 0).sum())
+        r.stamp_decisions += int((tr["pstar"] >= 0).sum())
+        r.stamps += int((tr["pstar"] > 1e-4).sum())
+        compare_sampled(layer, orc, units, 1e-4, tr["pstar"], r)
+    for r in (res, tail):
+        assert r.band_events == 0 and r.max_err <= OUT_TOL
+    rate = tail.stamps / tail.stamp_decisions
+    assert STAMP_BAND[0] <= rate <= STAMP_BAND[1], f"bench stream stamp rate {rate:.3f}"
+    assert tail.evictions >= len(units) * (48 // PAGE)
     assert layer.raas_get_status() == 0
 
 
@@ -490,6 +551,7 @@ def _long_prompt_stream(seed, B, Hq, Hkv, d, P, T):
     (2, 8, 2, 128, 512, 200, 640, 6, 0),     # 32 prompt pages, 6 attended per step
     (2, 28, 4, 128, 256, 160, 384, 4, 8),    # Qwen group, 16 prompt pages
     (1, 4, 2, 64, 160, 120, 256, 3, 0),      # d = 64, 10 prompt pages
+    (2, 8, 2, 128, 200, 120, 320, 4, 0),     # P % 16 = 8: partial last prompt page (always attended)
 ])
 def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp):
     """quest_prefill_pages = K (PAPER.md :173/:183, :237): GPU vs oracle, bit-exact state and
@@ -510,6 +572,45 @@ def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp
     # selection (the data are seeded, so this holds or fails deterministically)
     assert gaps and min(gaps) > 2e-6, "selection boundary too close for an fp32-vs-fp64 check"
     assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions > 0
+
+
+@pytest.mark.parametrize("kw,P,n1", [
+    ({"quest_prefill_pages": 4}, 200, 5),     # hybrid, the partial prompt page still filling
+    ({"quest_prefill_pages": 4}, 200, 40),    # hybrid, the partial prompt page full of decode tokens
+    ({}, 40, 3),                              # default method, cur = the pinned partial page
+    ({}, 40, 157),                            # default method, cur = a partial decode page
+    ({"page": 1}, 20, 77),                    # token level (deferred stamps flushed by get_state)
+    ({"stamp_rule": 1, "top_r": 0.5, "table_scope": 1}, 24, 101),
+])
+def test_set_state_roundtrip_continues_bitwise_gpu(kw, P, n1):
+    """get_state + get_kv -> set_state into a FRESH handle continues bitwise as the
+    uninterrupted handle (outputs, state, KV store) -- the GPU half of the resync the parity
+    protocol rests on.  The pinned flag 2 of a partial last prompt page keeps the hybrid's
+    selectable set (it used to become selectable after a round trip)."""
+    B, Hq, Hkv, d, T = 2, 8, 2, 128, 140 + n1
+    L = 320 if "quest_prefill_pages" in kw else (64 if kw.get("page") == 1 else 128)
+    st = waterfall_stream(4500 + P + n1, B, Hq, Hkv, d, P, T, p_phoenix=1.0 / 16, phoenix_len=8)
+    a = RaasLayer(L, 1e-4, Hq, Hkv, d, B, **kw)
+    a.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
+    out_a = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
+    out_b = torch.empty_like(out_a)
+    for i in range(n1):
+        a.raas_decode_step(to_dev(st.q[i]), to_dev(st.k[i]), to_dev(st.v[i]), out_a)
+    s = a.raas_get_state()
+    if P % PAGE and kw.get("page", 16) == 16:
+        assert (s["pinned"][:, P // PAGE] == 2).all()
+    ks, vs = a.raas_get_kv()
+    b = RaasLayer(L, 1e-4, Hq, Hkv, d, B, **kw)
+    b.raas_set_state(s["t"], s["ts"], s["start"], s["count"], s["pinned"], ks, vs)
+    for i in range(n1, T):
+        for ly, o in ((a, out_a), (b, out_b)):
+            ly.raas_decode_step(to_dev(st.q[i]), to_dev(st.k[i]), to_dev(st.v[i]), o)
+        assert torch.equal(out_a, out_b), f"out differs at step {i}"
+    sa, sb = a.raas_get_state(), b.raas_get_state()
+    assert all(np.array_equal(sa[k], sb[k]) for k in sa)
+    for x, y in zip(a.raas_get_kv(), b.raas_get_kv()):
+        assert np.array_equal(x, y)
+    assert a.raas_get_counters()["evictions"] > 0
 
 
 # ------------------------------------------------------------------ NEXT-2: one table per request
@@ -617,7 +718,8 @@ def test_token_level_alpha_extremes(oracle_mod, alpha):
 @pytest.mark.parametrize("kw", [
     {}, {"score_mode": 1}, {"stamp_rule": 1, "top_r": 0.5}, {"table_scope": 1},
     {"page": 1}, {"page": 1, "stamp_rule": 1, "top_r": 0.5}, {"quest_prefill_pages": 1},
-], ids=["default", "quest", "top_r", "table", "token_tokd", "token_top_r", "hybrid"])
+    {"disable_early_start": 1},
+], ids=["default", "quest", "top_r", "table", "token_tokd", "token_top_r", "hybrid", "no_early"])
 def test_interleaved_handles_early_start_matches_single_handle_runs(kw):
     """Layers interleaved on one stream (the model's order) take the early-start path: each
     launch reads its handle's state before griddepcontrol.wait, since the previous kernel is

@@ -10,7 +10,8 @@ torch = pytest.importorskip("torch")
 import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
-from paper_2502_11147_b200.shard import gather_heads, head_range, max_over_ranks, request_range  # noqa: E402
+from paper_2502_11147_b200.shard import (HeadGather, gather_heads, head_range,  # noqa: E402
+                                         max_over_ranks, request_range)
 
 
 def test_request_range_partitions():
@@ -57,6 +58,17 @@ def _worker(rank, world, port, q):
         _, _, ql, qh = head_range(2, Hq, world, rank)
         got = gather_heads(full[:, ql:qh].contiguous())
         ok_gather = torch.equal(got, full)
+        # the preallocated gather (the bench's head-sharded step): same result, same buffer
+        # every call (nothing allocated per layer-step), B = 1 and B > 1 layouts
+        ok_pre = True
+        for Bg in (1, 3):
+            fullg = torch.arange(Bg * Hq * d, dtype=torch.float32).reshape(Bg, Hq, d)
+            hg = HeadGather(Bg, qh - ql, d, torch.float32, "cpu")
+            buf = hg.full.data_ptr()
+            for rep in range(2):
+                got2 = hg(fullg[:, ql:qh].contiguous() + rep)
+                ok_pre &= torch.equal(got2, fullg + rep) and got2.data_ptr() == buf
+        ok_gather = ok_gather and ok_pre
         # request shards cover the batch exactly once
         lo, hi = request_range(64, world, rank)
         cover = torch.zeros(64, dtype=torch.int64)

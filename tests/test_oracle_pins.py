@@ -301,7 +301,7 @@ def test_p5_bookkeeping_enumeration(oracle_mod, page, P, L, T):
         for i, (snap, ev) in enumerate(ref):
             state, evs = got[i]
             mine = list(zip(state["start"][u].tolist(), state["count"][u].tolist(),
-                            np.where(state["pinned"][u] == 1, 0, state["ts"][u]).tolist()))
+                            np.where(state["pinned"][u] != 0, 0, state["ts"][u]).tolist()))
             assert mine == snap, (u, i)
             assert evs[u] == ev, (u, i)
 
@@ -758,3 +758,131 @@ def test_bench_waterfall_generator_is_selective(oracle_mod):
     rate = float(np.mean(stamped))
     assert n_ev > 0
     assert 0.05 < rate < 0.95, rate
+
+
+# ---------------------------------------------------------------- resync: set_state(get_state)
+
+
+def _roundtrip_case(oracle_mod, st, n1, check_split, **cfg):
+    """Run the oracle n1 steps, read its whole state (metadata + K/V stores), set it into a FRESH
+    oracle and continue both for the rest of the stream: states, stores and outputs must stay
+    bitwise identical (the lockstep resync of SURVEY §8c parity protocol rests on this).
+    `check_split(state)` asserts the property of the split point the case is about."""
+    B, _, P, d = st.k_pre.shape
+    a = oracle_mod.Oracle(head_dim=d, batch=B, **cfg)
+    a.prefill(st.k_pre, st.v_pre, P)
+    for i in range(n1):
+        a.decode_step(st.q[i], st.k[i], st.v[i])
+    s = a.get_state()
+    check_split(s)
+    ks, vs = a.get_kv()
+    b = oracle_mod.Oracle(head_dim=d, batch=B, **cfg)
+    b.set_state(s["t"], s["ts"], s["start"], s["count"], s["pinned"], ks, vs)
+    s_b = b.get_state()
+    for k in s:
+        assert np.array_equal(s[k], s_b[k]), k
+    evictions = 0
+    for i in range(n1, st.T):
+        oa = a.decode_step(st.q[i], st.k[i], st.v[i])
+        ob = b.decode_step(st.q[i], st.k[i], st.v[i])
+        assert np.array_equal(oa, ob), f"out differs at step {i}"
+        sa, sb = a.get_state(), b.get_state()
+        for k in sa:
+            assert np.array_equal(sa[k], sb[k]), f"state '{k}' differs at step {i}"
+        evictions += int((a.get_trace()["evicted"] >= 0).sum())
+    ka, va = a.get_kv()
+    kb, vb = b.get_kv()
+    assert np.array_equal(ka, kb) and np.array_equal(va, vb)
+    return evictions
+
+
+def _cur_page(s, u):
+    """the write page: the used page with the largest start position (the page of token t)"""
+    used = np.nonzero(s["count"][u] > 0)[0]
+    return used[np.argmax(s["start"][u][used])]
+
+
+@pytest.mark.parametrize("P,n1,where", [
+    (40, 3, "partial prompt page"),       # 40 % 16 = 8: decode tokens 41.. fill the pinned page 2
+    (40, 157, "partial decode page"),     # after evictions, cur = a victim page being refilled
+    (32, 160, "full page"),               # (32 + 160) % 16 == 0: the next step opens a page
+])
+def test_set_state_roundtrip_continues_bitwise(oracle_mod, P, n1, where):
+    """raas_ref_set_state re-derives the write cursor (the used page with the largest start
+    position), the used count and the pinned set from the metadata alone.  From a state whose
+    current page is partial (prompt or decode) or full, the resynced oracle must continue
+    exactly as the uninterrupted one (App. B :394-396: time, prompt pinning, eviction
+    of the earliest recorded time)."""
+    st = waterfall_stream(4100 + P + n1, 2, 8, 2, 64, P, 260)
+    cfg = dict(L=128, alpha=1e-4, page=PAGE, n_q_heads=8, n_kv_heads=2)
+
+    def check(s):
+        for u in range(4):
+            cur = _cur_page(s, u)
+            full = s["count"][u, cur] == PAGE
+            if where == "full page":
+                assert full
+            else:
+                assert not full
+                assert bool(s["pinned"][u, cur]) == (where == "partial prompt page")
+        if P % PAGE:
+            assert (s["pinned"][:, P // PAGE] == 2).all() and (s["pinned"][:, : P // PAGE] == 1).all()
+
+    assert _roundtrip_case(oracle_mod, st, n1, check, **cfg) > 0
+
+
+def test_set_state_roundtrip_token_level(oracle_mod):
+    """page = 1 (§3.2): every token its own entry; resync mid-stream after evictions."""
+    st = waterfall_stream(4200, 1, 4, 2, 64, 20, 200)
+    cfg = dict(L=64, alpha=1e-3, page=1, n_q_heads=4, n_kv_heads=2)
+    assert _roundtrip_case(oracle_mod, st, 77, lambda s: None, **cfg) > 0
+
+
+@pytest.mark.parametrize("n1", [5, 40])
+def test_set_state_roundtrip_hybrid_partial_prompt_page(oracle_mod, n1):
+    """Quest-on-prefill hybrid (D24) with P % 16 != 0: the prompt's partial last page is flagged
+    2 by get_state, never selectable, and always attended -- also after it has been filled by
+    decode tokens (n1 = 40) -- so the resynced run attends the same pages.  Taking every pinned
+    page as selectable, or none, changes the attended set and therefore out."""
+    P, K = 200, 4            # 12 full prompt pages + 8 prompt tokens in page 12
+    st = waterfall_stream(4300 + n1, 2, 8, 2, 64, P, 100, p_phoenix=1.0 / 16, phoenix_len=8)
+    cfg = dict(L=320, alpha=1e-4, page=PAGE, n_q_heads=8, n_kv_heads=2, quest_prefill_pages=K)
+
+    def check(s):
+        assert (s["pinned"][:, :12] == 1).all() and (s["pinned"][:, 12] == 2).all()
+        assert (s["count"][:, 12] == (PAGE if n1 >= 8 else 8 + n1)).all()
+
+    _roundtrip_case(oracle_mod, st, n1, check, **cfg)
+
+
+def test_set_state_roundtrip_request_table_top_r(oracle_mod):
+    """One table per request (D25) with the top-r rule (D23): the replicas resync as one."""
+    st = waterfall_stream(4400, 2, 8, 2, 64, 24, 220)
+    cfg = dict(L=96, alpha=1e-4, page=PAGE, n_q_heads=8, n_kv_heads=2, stamp_rule=1, top_r=0.5,
+               table_scope=1)
+    assert _roundtrip_case(oracle_mod, st, 101, lambda s: None, **cfg) > 0
+
+
+def test_set_state_hybrid_flags_select_the_full_prompt_pages(oracle_mod):
+    """The pinned flags are what set_state derives the hybrid's selectable pages from: a state
+    read from an uninterrupted run but with the partial page re-flagged 1 (i.e. 'every pinned
+    page is a full prompt page') must NOT continue like the original -- the check above would be
+    vacuous otherwise."""
+    P, K = 200, 4
+    st = waterfall_stream(4340, 2, 8, 2, 64, P, 100, p_phoenix=1.0 / 16, phoenix_len=8)
+    cfg = dict(L=320, alpha=1e-4, page=PAGE, n_q_heads=8, n_kv_heads=2, quest_prefill_pages=K)
+    a = oracle_mod.Oracle(head_dim=64, batch=2, **cfg)
+    a.prefill(st.k_pre, st.v_pre, P)
+    for i in range(40):
+        a.decode_step(st.q[i], st.k[i], st.v[i])
+    s = a.get_state()
+    ks, vs = a.get_kv()
+    b = oracle_mod.Oracle(head_dim=64, batch=2, **cfg)
+    bad = dict(s, pinned=np.where(s["pinned"] == 2, 1, s["pinned"]).astype(np.uint8))
+    b.set_state(bad["t"], bad["ts"], bad["start"], bad["count"], bad["pinned"], ks, vs)
+    differs = False
+    for i in range(40, st.T):
+        oa = a.decode_step(st.q[i], st.k[i], st.v[i])
+        ob = b.decode_step(st.q[i], st.k[i], st.v[i])
+        differs |= not np.array_equal(oa, ob)
+    assert differs
