@@ -584,7 +584,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                      # the committed ncu capture is of the default variant of the workload
                      "traffic": None if variant else ncu_traffic(cfg["workload"]),
                      "kernel": f"raas_decode_kernel<{d},8,16> grid {info['grid']} x {info['block']} thr, "
-                               f"{info['smem']} B smem, {info['split_pages']}-page splits",
+                               f"{info['smem']} B smem, {info['split_pages']}-page splits"
+                               + (f", clusters of {info['cluster']} (partials via DSMEM)" if info['cluster'] > 1 else ""),
                      "algorithmic_bytes_per_launch": bytes_launch,
                      "avg_launch_us": launch_s * 1e6, "peak_source": peak_src,
                      "timing": "CUDA events on the launch stream around K graph replays of "

@@ -209,8 +209,10 @@ RAAS_API int raas_get_status(raas_handle* h, void* stream);
 RAAS_API int raas_get_counters(raas_handle* h, uint64_t counters[4], void* stream);
 
 /* Launch shape of the decode kernel (for roofline accounting): grid CTAs, threads per CTA,
- * dynamic shared memory bytes, split pages, splits per unit. */
-RAAS_API int raas_launch_info(const raas_handle* h, int32_t info[5]);
+ * dynamic shared memory bytes, split pages, splits per unit, thread-block cluster size (1: the
+ * default persistent schedule; nsplit: the cluster schedule for small batches, where each
+ * unit's split CTAs exchange their partials through distributed shared memory). */
+RAAS_API int raas_launch_info(const raas_handle* h, int32_t info[6]);
 
 /* Thread-local message describing the last error (never NULL). */
 RAAS_API const char* raas_last_error(void);

@@ -49,8 +49,8 @@ size_t up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 #endif
 constexpr int NC = RAAS_NC;  // consumer (MMA) warps per CTA
 constexpr int S = RAAS_S;    // K+V page stages in the ring (8 KiB each at head_dim 128)
-template <int D, bool TOKD = false>
-using Lay = raas::DecodeLayout<D, NC, S, TOKD>;
+template <int D, bool TOKD = false, bool GEN = false>
+using Lay = raas::DecodeLayout<D, NC, S, TOKD, GEN>;
 // three instantiations: the default method (lean), every option at run time (gen), and the
 // deferred token level (tokd)
 template <int D, bool TOKD, bool GEN>
@@ -68,7 +68,9 @@ struct Derived {
   int tokd;    // token level with deferred stamping (page 1, threshold rule, per-head tables)
   int gen;     // any option beyond the default method (page 16, exact score, alpha rule,
                // per-kv-head tables, no Quest-on-prefill): the generic kernel instantiation
-  int pstr;    // bf16 elements per KV page: 2 * 16 * D, + 64 (ts/start trailer) when tokd
+  int pstr;    // bf16 elements per KV page: 2 * 16 * D, + 64 (ts/start trailer) when tokd,
+               // + 2 * D (the Quest mode's per-channel min / max key rows) when score_mode 1
+  int qtr;     // score_mode 1 at page 16: min / max rows maintained in the page trailer
 };
 
 int derive(const raas_config* c, Derived* d) {
@@ -90,7 +92,8 @@ int derive(const raas_config* c, Derived* d) {
   d->ep = c->page;
   d->Ce = c->L / c->page;
   d->tokd = c->page == 1 && c->stamp_rule == 0 && c->table_scope == 0 && c->score_mode == 0;
-  d->pstr = 2 * raas::PAGE * c->head_dim + (d->tokd ? 64 : 0);
+  d->qtr = c->score_mode == 1 && c->page == raas::PAGE;
+  d->pstr = 2 * raas::PAGE * c->head_dim + (d->tokd ? 64 : 0) + (d->qtr ? 2 * c->head_dim : 0);
   d->gen = !d->tokd && (c->page != raas::PAGE || c->score_mode != 0 || c->stamp_rule != 0 ||
                         c->table_scope != 0 || c->quest_prefill_pages > 0);
   if (c->page == 1 && c->score_mode != 0)
@@ -222,6 +225,7 @@ struct raas_handle {
   int device;
   int num_sms;
   int grid;
+  int cl;  // cluster schedule (DecodeParams::cl): grid = units * nsplit, clusters of nsplit
   int smem;
   uint8_t* arena;
   int prefilled;
@@ -300,6 +304,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
     // the caller opted out (raas.h "Early start")
     p.early = (other || after_copies) && h->cfg.quest_prefill_pages == 0 && !h->cfg.disable_early_start;
   }
+  p.cl = h->cl;
   p.n_kv = h->cfg.n_kv_heads;
   p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;
   p.req_ctr = h->cfg.table_scope ? reinterpret_cast<int32_t*>(a + h->lay.req_ctr) : nullptr;
@@ -329,11 +334,15 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   lc.blockDim = dim3(Lay<D>::THREADS);  // the same for both instantiations
   lc.dynamicSmemBytes = h->smem;
   lc.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = h->cl ? h->d.nsplit : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = h->cl ? 2 : 1;
   if (h->d.tokd)     RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true, false>(), p));
   else if (h->d.gen) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, true>(), p));
   else               RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, false>(), p));
@@ -368,15 +377,43 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
 template <int D, bool TOKD, bool GEN>
 int setup_kernel_t(raas_handle* h) {
   auto k = decode_kernel<D, TOKD, GEN>();
-  h->smem = Lay<D, TOKD>::SMEM;
+  h->smem = Lay<D, TOKD, GEN>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
-  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD>::THREADS, h->smem));
+  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD, GEN>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
   h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
   if (const char* e = std::getenv("RAAS_GRID")) {  // tuning experiments only (scripts/)
     const int G = std::atoi(e);
     if (G > 0) h->grid = std::min(G, h->num_sms * per_sm);
+  }
+  // Cluster schedule when the (unit, split) tiles fit the SMs one per CTA and every unit is
+  // split (small batches, e.g. config 2 at B = 1): each unit's nsplit CTAs form a cluster and
+  // hand their split partials to the leader through distributed shared memory instead of L2
+  // (publish + acq_rel counter + loads).  Numerics are the same as the default schedule's.
+  h->cl = 0;
+  const long long tiles = (long long)h->d.units * h->d.nsplit;
+  bool want = RAAS_CL && !TOKD && h->d.nsplit >= 2 && h->d.nsplit <= 8 && tiles <= h->num_sms * per_sm;
+  if (const char* e = std::getenv("RAAS_CLUSTER")) want = want && std::atoi(e) != 0;  // A/B only
+  if (want) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)tiles);
+    lc.blockDim = dim3(Lay<D, TOKD, GEN>::THREADS);
+    lc.dynamicSmemBytes = h->smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = h->d.nsplit;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, k, &lc) == cudaSuccess && nclusters > 0) {
+      h->cl = 1;
+      h->grid = (int)tiles;
+    } else {
+      cudaGetLastError();  // clusters of this size do not fit: keep the default schedule
+    }
   }
   return RAAS_OK;
 }
@@ -395,9 +432,26 @@ int build_repkeys(raas_handle* h, cudaStream_t st) {
   auto* rk = reinterpret_cast<__nv_bfloat16*>(a + h->lay.repkey);
   auto* nf = reinterpret_cast<const int32_t*>(a + h->lay.nfull);
   if (h->cfg.head_dim == 128)
-    raas::raas_repkey_kernel<128><<<blocks, 256, 0, st>>>(kvs, rk, nf, h->d.units, h->d.C);
+    raas::raas_repkey_kernel<128><<<blocks, 256, 0, st>>>(kvs, rk, nf, h->d.units, h->d.C, h->d.pstr);
   else
-    raas::raas_repkey_kernel<64><<<blocks, 256, 0, st>>>(kvs, rk, nf, h->d.units, h->d.C);
+    raas::raas_repkey_kernel<64><<<blocks, 256, 0, st>>>(kvs, rk, nf, h->d.units, h->d.C, h->d.pstr);
+  RAAS_CUDA(cudaGetLastError());
+  return RAAS_OK;
+}
+
+// Quest score mode: rebuild every page's min / max trailer from the store (after prefill /
+// set_state; the decode kernel maintains them on write afterwards)
+int build_qtrailers(raas_handle* h, cudaStream_t st) {
+  if (!h->d.qtr) return RAAS_OK;
+  uint8_t* a = h->arena;
+  const size_t total = (size_t)h->d.units * h->d.C * (h->cfg.head_dim / 8);
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)h->num_sms * 16);
+  auto* kvs = reinterpret_cast<__nv_bfloat16*>(a + h->lay.kvstore);
+  auto* cnt = reinterpret_cast<const int32_t*>(a + h->lay.cnt);
+  if (h->cfg.head_dim == 128)
+    raas::raas_qtrailer_kernel<128><<<blocks, 256, 0, st>>>(kvs, cnt, h->d.units, h->d.C, h->d.pstr);
+  else
+    raas::raas_qtrailer_kernel<64><<<blocks, 256, 0, st>>>(kvs, cnt, h->d.units, h->d.C, h->d.pstr);
   RAAS_CUDA(cudaGetLastError());
   return RAAS_OK;
 }
@@ -558,6 +612,7 @@ int raas_prefill_varlen(raas_handle* h, const void* k, const void* v, const int3
       h->d.units, h->cfg.n_kv_heads, h->d.Ce, h->d.ep);
   RAAS_CUDA(cudaGetLastError());
   int rc = build_repkeys(h, st);
+  if (!rc) rc = build_qtrailers(h, st);
   if (!rc) rc = refresh(h, st);
   if (!rc) rc = tok_sync(h, st);
   if (rc) return rc;
@@ -743,6 +798,7 @@ int raas_set_state(raas_handle* h, const int32_t* t, const int32_t* ts, const in
     RAAS_CUDA(cudaMemcpyAsync(a + h->lay.kvstore, dev.data(), dev.size() * 2, cudaMemcpyHostToDevice, st));
   }
   int rc = build_repkeys(h, st);
+  if (!rc) rc = build_qtrailers(h, st);
   if (!rc) rc = refresh(h, st);
   if (!rc) rc = tok_sync(h, st);
   if (rc) return rc;
@@ -790,13 +846,14 @@ RAAS_API int raas_debug_tokd(int32_t* out16) {
   return cudaMemcpyFromSymbol(out16, raas::g_tokd_dbg, 64) == cudaSuccess ? 0 : 1;
 }
 #endif
-int raas_launch_info(const raas_handle* h, int32_t info[5]) {
+int raas_launch_info(const raas_handle* h, int32_t info[6]) {
   if (!h || !info) return fail(RAAS_E_INVALID, "null argument");
   info[0] = h->grid;
   info[1] = h->cfg.head_dim == 128 ? Lay<128>::THREADS : Lay<64>::THREADS;
   info[2] = h->smem;
   info[3] = h->d.split_pages;
   info[4] = h->d.nsplit;
+  info[5] = h->cl ? h->d.nsplit : 1;
   return RAAS_OK;
 }
 

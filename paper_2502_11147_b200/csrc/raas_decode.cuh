@@ -25,6 +25,12 @@
 //                  the <= 8 q-heads of the GQA group = N), online softmax in fp32 registers.
 #pragma once
 
+#ifndef RAAS_CL
+#define RAAS_CL 1  // compile the cluster schedule (DecodeParams::cl) into the kernels
+#endif
+#ifndef RAAS_DEP
+#define RAAS_DEP 2  // consumer deposit buffers per consumer (see DecodeLayout::NDEP)
+#endif
 #ifndef RAAS_PREFETCH_TILES
 #define RAAS_PREFETCH_TILES 4  // cap on the owned tiles warmed in L2 before griddepcontrol.wait
 #endif
@@ -64,6 +70,7 @@ __device__ __forceinline__ void dbg_add(int, long long) {}
     dbg_add(slot, t0_);                 \
   } while (0)
 
+constexpr int PUB_ACC_OFF = MAX_GROUP * 8;  // cluster schedule: acc after the (m, l) pairs
 constexpr int FLAG_FIRST = 1;  // first page of this tile for the consuming warp
 constexpr int FLAG_LAST = 2;   // last page of this tile for the consuming warp
 constexpr int FLAG_END = 4;    // no more work
@@ -92,17 +99,25 @@ __device__ __forceinline__ void merge_factors(float m, float ms, float& mn, floa
 // ("shared") units are grabbed dynamically from a global counter, so CTAs that streamed
 // faster take more of them and the kernel ends balanced.  The last CTA to exit resets the
 // counter for the next launch.
+// Cluster schedule (cl): CTA b streams tile b only, i.e. split b % nsplit of unit b / nsplit
+// (the cluster of the unit's nsplit consecutive CTAs).
 struct TileSched {
   int b, G, fu, nsplit, n_owned, n_shared_tiles, shared_base, i_owned;
-  __device__ TileSched(int units, int nsplit_, int G_, int b_) : b(b_), G(G_), nsplit(nsplit_) {
-    fu = units / G;
+  bool cl;
+  __device__ TileSched(int units, int nsplit_, int G_, int b_, bool cl_)
+      : b(b_), G(G_), nsplit(nsplit_), cl(cl_) {
+    fu = cl ? 0 : units / G;
     n_owned = fu * nsplit;
-    n_shared_tiles = (units - fu * G) * nsplit;
+    n_shared_tiles = cl ? 0 : (units - fu * G) * nsplit;
     shared_base = fu * G * nsplit;
     i_owned = 0;
   }
   // next tile for this CTA (warp-uniform), -1 when none is left
   __device__ int next(int* grab, int lane, bool& owned) {
+    if (cl) {
+      owned = false;
+      return i_owned++ == 0 ? b : -1;
+    }
     if (i_owned < n_owned) {
       owned = true;
       return b * n_owned + i_owned++;
@@ -169,18 +184,24 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
-template <int D, int NC, int S, bool TOKD = false>
+template <int D, int NC, int S, bool TOKD = false, bool QTR = false>
 struct DecodeLayout {
   static constexpr int KS = D / 16;
   static constexpr int TILE = PAGE * D * 2;  // one K (or V) page
-  static constexpr int STAGE = 2 * TILE + (TOKD ? 128 : 0);  // tokd: + the ts/start trailer
+  // tokd: + the ts/start trailer; QTR (the generic kernel): room for the Quest mode's per-page
+  // min / max key rows (2 x D bf16) that follow the page's V rows in HBM
+  static constexpr int STAGE = 2 * TILE + (TOKD ? 128 : 0) + (QTR ? 4 * D : 0);
   static constexpr int QBUF = MAX_GROUP * D * 2;
   static constexpr int FRAG = KS * 4 + 4;  // floats per lane in a consumer's deposit
   static constexpr int DEPOSIT = FRAG * 32 * 4;
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_Q = OFF_RING + S * STAGE;
   static constexpr int OFF_MERGE = OFF_Q + 2 * QBUF;
-  static constexpr int OFF_SCR = OFF_MERGE + 2 * NC * DEPOSIT;            // combine scratch
+  // consumer deposits: one buffer per consumer (RAAS_DEP 1: a consumer waits until the merge
+  // warp has read its previous tile's deposit; the smem goes to ring stages) or one per tile
+  // parity (RAAS_DEP 2)
+  static constexpr int NDEP = RAAS_DEP;
+  static constexpr int OFF_SCR = OFF_MERGE + NDEP * NC * DEPOSIT;         // combine scratch
   static constexpr int SCR = MAX_SPLITS * MAX_GROUP * 8 + 6 * MAX_GROUP * 4;
   static constexpr int OFF_SINFO = OFF_SCR + SCR;                          // int4[2] per stage
   static constexpr int OFF_TINFO = OFF_SINFO + S * 32;                     // int4[3] per parity
@@ -194,14 +215,19 @@ struct DecodeLayout {
   static constexpr int OFF_QP = OFF_CAND + (TOKD ? 2 * NC * 16 : 0);
   static constexpr int QPBUF = QBUF + 32;  // q_prev rows, then 8 floats of LSE
   static constexpr int OFF_BAR = (OFF_QP + (TOKD ? 2 * QPBUF : 0) + 127) / 128 * 128;
-  // After its END sentinel a consumer's two ring stages (w, w+NC) are never written again, so
-  // for D = 128 it joins the combine pool with stage w as its scratch (the kernel's tail is
-  // the combines of the last units: more poppers, shorter tail).
-  static constexpr bool JOIN = STAGE >= SCR && S == 2 * NC;
+  // After its END sentinel (the NC sentinels take NC consecutive ring positions, hence distinct
+  // stages) no stage is written again, so for D = 128 a consumer joins the combine pool with
+  // its sentinel's stage as scratch (the kernel's tail is the combines of the last units: more
+  // poppers, shorter tail).
+  static constexpr bool JOIN = STAGE >= SCR && S >= NC;
   static constexpr int NPOP = 1 + (JOIN ? NC : 0);
   static_assert(CQ >= NPOP, "a popper may wait at most one queue phase ahead");
-  // full[S], empty[S], qfull[2], mfull[2], tfree[2], cq_full[CQ], cq_empty[CQ]
-  static constexpr int NBAR = 2 * S + 6 + 2 * CQ;
+  // full[S], empty[S], qfull[2], mfull[2], tfree[2], cq_full[CQ], cq_empty[CQ], clfull
+  static constexpr int NBAR = 2 * S + 6 + 2 * CQ + 1;
+  // cluster schedule (p.cl): the tile's split partial, published in this CTA's merge area once
+  // the merge warp has read the (only) tile's deposits: float2 (m, l)[MAX_GROUP], then
+  // float acc[g][D]; read by the cluster's leader through distributed shared memory
+  static_assert(PUB_ACC_OFF + MAX_GROUP * D * 4 <= NDEP * NC * DEPOSIT, "publish area");
   static constexpr int BYTES = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = BYTES + 1024;  // + alignment slack
   static constexpr int THREADS = (NC + 3) * 32;  // producer, merge, combine, NC consumers
@@ -212,7 +238,13 @@ struct DecodeLayout {
 // ---------------------------------------------------------------------------------------------
 template <int D, bool GEN>
 __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, int nse, uint32_t scr,
-                                             int lane, bool outdone) {
+                                             int lane, bool outdone, bool CL = false, uint32_t pub = 0,
+                                             uint32_t clbar = 0) {
+  // CL (cluster schedule): split s's partial is in the merge area of the cluster's CTA s
+  // (`pub`, read through distributed shared memory) once every CTA's merge warp has arrived
+  // on the leader's `clbar` (release / acquire at cluster scope); the arithmetic below is the
+  // same as for partials read from L2, so results do not depend on the schedule
+  if (CL) mbar_wait_cluster(clbar, 0);
   // outdone: the merge warp already folded the splits and wrote out; the LSE is in scr_lse
   // GEN = false: the default method (page = 16, alpha rule, one table per kv-head) with the
   // optional rules compiled out; GEN = true: every option decided at run time
@@ -233,7 +265,8 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = 32 * k + lane;
-    mla[k] = (!outdone && i < NE) ? __ldcg(ml_g + i) : make_float2(-INFINITY, 0.f);
+    mla[k] = (outdone || i >= NE) ? make_float2(-INFINITY, 0.f)
+             : CL ? ld_dsmem_f32x2(mapa(pub + 8 * (i % g), i / g)) : __ldcg(ml_g + i);
   }
   // page metadata for a6/a7 (bounded by C, masked by the plan's page count later)
   constexpr int PPL = 4;  // pages per lane per chunk
@@ -275,10 +308,12 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     for (int i = 0; i < CB; ++i) {
       const int c = lane + 32 * (cb + i), h = c / CPH, d4 = c - h * CPH;
 #pragma unroll
-      for (int u = 0; u < SG; ++u)
-        v[i][u] = (!outdone && c < nch && s0 + u < nse)
-                      ? __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < SG; ++u) {
+        const bool ok = !outdone && c < nch && s0 + u < nse;
+        v[i][u] = !ok ? make_float4(0.f, 0.f, 0.f, 0.f)
+                  : CL ? ld_dsmem_f32x4(mapa(pub + PUB_ACC_OFF + (h * D + 4 * d4) * 4, s0 + u))
+                       : __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4);
+      }
     }
   };
   load_acc(0, 0);
@@ -290,7 +325,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       if (i < NE) { sts_f32(scr_w + 8 * i, mla[k].x); sts_f32(scr_w + 8 * i + 4, mla[k].y); }
     }
     for (int i = 64 + lane; i < NE; i += 32) {  // more than 64 (split, head) pairs
-      const float2 ml = __ldcg(ml_g + i);
+      const float2 ml = CL ? ld_dsmem_f32x2(mapa(pub + 8 * (i % g), i / g)) : __ldcg(ml_g + i);
       sts_f32(scr_w + 8 * i, ml.x);
       sts_f32(scr_w + 8 * i + 4, ml.y);
     }
@@ -657,7 +692,7 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 __device__ int g_tokd_dbg[16];
 #endif
 template <int D, int NC, int S, bool TOKD, bool GEN>
-__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
   // GEN = false (and !TOKD): the default method only (page = 16, exact page score, alpha rule,
   // per-kv-head tables, no Quest-on-prefill); the options' run-time branches are compiled out
@@ -666,7 +701,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
   // TOKD: the deferred token-level instantiation (p.tokd == 1); the page kernel carries none
   // of its code
   static_assert(D == 64 || D == 128, "head_dim");
-  using Lay = DecodeLayout<D, NC, S, TOKD>;
+  using Lay = DecodeLayout<D, NC, S, TOKD, GEN>;
   constexpr int KS = Lay::KS, TILE = Lay::TILE, STAGE = Lay::STAGE;
   constexpr int ROW = 2 * D;  // bytes per token row
 
@@ -690,6 +725,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
   auto tfree = [&](int par) { return bar + 8 * (2 * S + 4 + par); };
   auto cqfull = [&](int q) { return bar + 8 * (2 * S + 6 + q); };
   auto cqempty = [&](int q) { return bar + 8 * (2 * S + 6 + CQ + q); };
+  const uint32_t clfull = bar + 8 * (2 * S + 6 + 2 * CQ);  // cluster schedule: partials published
+  const bool cl = RAAS_CL && !TOKD && p.cl != 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef RAAS_DBG_TIMING
@@ -709,10 +746,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       mbar_init(cqfull(q), 1);
       mbar_init(cqempty(q), 1);
     }
+    if (cl) mbar_init(clfull, p.nsplit * 32);  // every lane of every merge warp of the cluster
     *pop_ctr = 0;
     fence_mbar_init();
   }
   __syncthreads();
+  if (cl) cluster_sync_all();  // the leader's barrier is initialised before any remote arrival
   if (warp == 0 && quest_k == 0) {
     // Warm L2 with this CTA's first owned tile while the previous kernel drains (its tail
     // leaves HBM idle).  Only a hint: nothing is read from these lines before griddepcontrol.wait
@@ -782,7 +821,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
       if constexpr (TOKD) combine_unit_tok<D>(p, unit, nse_u, scratch, lane);
-      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane, outdone);
+      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane, outdone, cl, merge, clfull);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -848,13 +887,15 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
         sinfo[2 * s] = make_int4(unit, page, (is_slot && !tok) ? off + 1 : c, patch);
         sinfo[2 * s + 1] =
             make_int4(kt, (i < NC ? FLAG_FIRST : 0) | (i + NC >= n ? FLAG_LAST : 0), 0, 0);
-        mbar_arrive_expect_tx(full(s), STAGE);  // tokd: the trailer comes with the page
+        // the whole HBM page (pstr elements: K rows, V rows, and the tokd ts/start trailer or
+        // the Quest min / max rows when the handle has one)
+        mbar_arrive_expect_tx(full(s), p.pstr * 2);
         bulk_load_hint(ring + s * STAGE, p.kvstore + (size_t)(unit * C + page) * p.pstr,
-                       STAGE, full(s), pol);
+                       p.pstr * 2, full(s), pol);
       }
       __syncwarp();
     };
-    TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x);
+    TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x, cl);
     bool owned = false, owned_next = false;
     int tile = sched.next(p.sched, lane, owned);
     if (tile >= 0) fetch(tile);
@@ -989,13 +1030,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       for (int i = 0; i < KS * 4; ++i) acc[i] = 0.f;
       float M0 = -INFINITY, M1 = -INFINITY, L0 = 0.f, L1 = 0.f;
       for (int i = 0; i < nw; ++i) {
-        const uint32_t dep = merge + (par * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
+        const uint32_t dep = merge + ((par % Lay::NDEP) * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
         M0 = fmaxf(M0, lds_f32(dep + 128 * (KS * 4 + 0)));
         M1 = fmaxf(M1, lds_f32(dep + 128 * (KS * 4 + 1)));
       }
       const float M0b = M0 == -INFINITY ? 0.f : M0, M1b = M1 == -INFINITY ? 0.f : M1;  // empty tile
       for (int i = 0; i < nw; ++i) {
-        const uint32_t dep = merge + (par * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
+        const uint32_t dep = merge + ((par % Lay::NDEP) * NC + (J + i) % NC) * Lay::DEPOSIT + 4 * lane;
         const float s0 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 0)) - M0b);
         const float s1 = fast_exp2(lds_f32(dep + 128 * (KS * 4 + 1)) - M1b);
         L0 += s0 * lds_f32(dep + 128 * (KS * 4 + 2));
@@ -1069,6 +1110,24 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
         }
         continue;
       }
+      if (cl) {
+        // cluster schedule: the partial goes to this CTA's merge area (its deposits are read:
+        // the tile was the CTA's only one), then every lane arrives on the leader's barrier;
+        // the leader's combine reads all splits' partials through distributed shared memory
+        if (lane < 4) {
+          if (2 * qd < g) sts_f32(merge + 8 * (2 * qd), M0), sts_f32(merge + 8 * (2 * qd) + 4, L0);
+          if (2 * qd + 1 < g) sts_f32(merge + 8 * (2 * qd + 1), M1), sts_f32(merge + 8 * (2 * qd + 1) + 4, L1);
+        }
+        const uint32_t pa0 = merge + PUB_ACC_OFF + ((2 * qd) * D + r) * 4, pa1 = pa0 + D * 4;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          if (2 * qd < g) { sts_f32(pa0 + 64 * mt, acc[4 * mt + 0]); sts_f32(pa0 + 64 * mt + 32, acc[4 * mt + 2]); }
+          if (2 * qd + 1 < g) { sts_f32(pa1 + 64 * mt, acc[4 * mt + 1]); sts_f32(pa1 + 64 * mt + 32, acc[4 * mt + 3]); }
+        }
+        mbar_arrive_remote(mapa(clfull, 0));
+        if (cluster_ctarank() == 0) push(unit | nse << CQ_UNIT_BITS);
+        continue;
+      }
       // publish the tile's split-K partial (m, l, acc) in the C-fragment layout
       const int pbase = (unit * p.nsplit + split) * g;
       if (TOKD && lane == 0) p.part_key[unit * p.nsplit + split] = ck;
@@ -1134,7 +1193,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
             atomicAdd(p.stats + 1, (unsigned long long)n_dec);
           }
         }
-        if constexpr (Lay::JOIN) combine_loop(ring + w * STAGE);  // join the tail's combines
+        if constexpr (Lay::JOIN) combine_loop(ring + s * STAGE);  // join the tail's combines
         break;
       }
       if (flags & FLAG_SKIP) {
@@ -1210,6 +1269,34 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
                        : "memory");
           *reinterpret_cast<uint4*>(p.kvstore + (size_t)(unit * C + page) * p.pstr +
                                     ((isv ? PAGE : 0) + patch) * D + phys * 8) = val;
+          if (GEN && score_mode == 1 && !isv) {
+            // the page's per-channel min / max rows (Quest representative keys, maintained on
+            // write): a fresh page (row 0) restarts them from the new key
+            const uint32_t ta = kb + 2 * TILE + ch * 16;
+            uint4 mn = val, mx = val;
+            if (patch > 0) {
+              uint4 omn, omx;
+              asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(omn.x), "=r"(omn.y), "=r"(omn.z), "=r"(omn.w) : "r"(ta));
+              asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(omx.x), "=r"(omx.y), "=r"(omx.z), "=r"(omx.w) : "r"(ta + 2 * D));
+              asm("min.bf16x2 %0, %0, %1;" : "+r"(mn.x) : "r"(omn.x));
+              asm("min.bf16x2 %0, %0, %1;" : "+r"(mn.y) : "r"(omn.y));
+              asm("min.bf16x2 %0, %0, %1;" : "+r"(mn.z) : "r"(omn.z));
+              asm("min.bf16x2 %0, %0, %1;" : "+r"(mn.w) : "r"(omn.w));
+              asm("max.bf16x2 %0, %0, %1;" : "+r"(mx.x) : "r"(omx.x));
+              asm("max.bf16x2 %0, %0, %1;" : "+r"(mx.y) : "r"(omx.y));
+              asm("max.bf16x2 %0, %0, %1;" : "+r"(mx.z) : "r"(omx.z));
+              asm("max.bf16x2 %0, %0, %1;" : "+r"(mx.w) : "r"(omx.w));
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "r"(mn.x), "r"(mn.y),
+                         "r"(mn.z), "r"(mn.w) : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta + 2 * D), "r"(mx.x),
+                         "r"(mx.y), "r"(mx.z), "r"(mx.w) : "memory");
+            __nv_bfloat16* tg = p.kvstore + (size_t)(unit * C + page) * p.pstr + 2 * PAGE * D;
+            *reinterpret_cast<uint4*>(tg + ch * 8) = mn;
+            *reinterpret_cast<uint4*>(tg + D + ch * 8) = mx;
+          }
           fence_proxy_async_smem();  // before the stage is refilled by TMA
         }
         __syncwarp();
@@ -1330,24 +1417,20 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
       if (score_mode == 1) {
         // Quest's representative-key bound (PAPER.md :147-151, :362; reading D22): per channel
         // c, max(q_c min_c, q_c max_c) over the page's valid keys, summed over c.  Lane l owns
-        // channels [l*CQ, (l+1)*CQ); the page is already in shared memory (no extra HBM bytes).
+        // channels [l*CQ, (l+1)*CQ).  The per-channel min / max rows ("a representative key
+        // (K) for each page", :147) are maintained on write and arrive with the page (+2 rows
+        // per 32 K/V rows of bytes), so no key row is scanned here.
         constexpr int CQL = D / 32;
-        const int c0 = lane * CQL, chk = c0 >> 3, wi = c0 & 7;
-        uint32_t mnp[CQL / 2], mxp[CQL / 2];  // packed bf16x2 running min / max (exact)
-#pragma unroll
-        for (int i = 0; i < CQL / 2; ++i) { mnp[i] = 0x7f807f80u; mxp[i] = 0xff80ff80u; }
-        for (int row = 0; row < cnt; ++row) {
-          const uint32_t a = kb + row * ROW + ((chk ^ (row & 7)) << 4) + wi * 2;
-          uint32_t w[CQL / 2];
+        const int c0 = lane * CQL;
+        uint32_t mnp[CQL / 2], mxp[CQL / 2];  // packed bf16x2 min / max (exact)
+        {
+          const uint32_t a = kb + 2 * TILE + c0 * 2;
           if constexpr (CQL == 4) {
-            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(a));
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(mnp[0]), "=r"(mnp[1]) : "r"(a));
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(mxp[0]), "=r"(mxp[1]) : "r"(a + 2 * D));
           } else {
-            w[0] = lds_u32(a);
-          }
-#pragma unroll
-          for (int i = 0; i < CQL / 2; ++i) {
-            asm("min.bf16x2 %0, %0, %1;" : "+r"(mnp[i]) : "r"(w[i]));
-            asm("max.bf16x2 %0, %0, %1;" : "+r"(mxp[i]) : "r"(w[i]));
+            mnp[0] = lds_u32(a);
+            mxp[0] = lds_u32(a + 2 * D);
           }
         }
         release_stage();  // the page's rows are no longer needed
@@ -1448,7 +1531,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
           l0 += __shfl_xor_sync(0xffffffffu, l0, o);
           l1 += __shfl_xor_sync(0xffffffffu, l1, o);
         }
-        const uint32_t dep = merge + (par * NC + w) * Lay::DEPOSIT + 4 * lane;
+        if constexpr (Lay::NDEP == 1) {
+          // single deposit buffer: tile k - 1's deposits must have been read by the merge warp
+          // (tfree of tile k - 1 = phase (k - 1) >> 1 of tfree((k - 1) & 1))
+          if (k > 0) RAAS_TIMED(3, mbar_wait(tfree((k - 1) & 1), ((k - 1) >> 1) & 1));
+        }
+        const uint32_t dep = merge + ((par % Lay::NDEP) * NC + w) * Lay::DEPOSIT + 4 * lane;
 #pragma unroll
         for (int mt = 0; mt < KS; ++mt)
 #pragma unroll
@@ -1472,6 +1560,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD>::THREADS, 1)
   // the last CTA out resets the dynamic-schedule counter for the next launch (which reads it
   // only after griddepcontrol.wait, i.e. after this grid has completed)
   __syncthreads();
+  if (cl) cluster_sync_all();  // the leader has read every CTA's partial: they may exit
 #ifdef RAAS_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 256) g_raas_tl[p.dbg_slot & 7][blockIdx.x][3] = dbg_gtimer();
 #endif

@@ -69,6 +69,9 @@ struct DecodeParams {
   int table_scope;       // 0 per (request, kv-head) tables; 1 one table per request (D25)
   int n_kv;              // kv-heads per request (units of one request are consecutive)
   int dbg_slot;          // RAAS_DBG_TIMING builds: timeline slot of this launch (0..7)
+  int cl;                // 1: cluster schedule -- one (unit, split) tile per CTA, the unit's nsplit
+                         // CTAs form a thread-block cluster, the split partials go to the leader
+                         // (cluster rank 0) through distributed shared memory, no L2 round trip
   int early;             // 1: the previous kernel of the stream is not this handle's decode step,
                          // so this handle's state may be read before griddepcontrol.wait
   uint32_t* req_x;       // [batch][C] table_scope 1: order-preserving max of the page scores
@@ -350,12 +353,43 @@ __global__ void raas_tok_trailer_sync(__nv_bfloat16* kvstore, const int32_t* __r
 // ------------------------------------------------------------------------------------------
 // Quest-on-prefill + RaaS-on-decode hybrid (SURVEY NEXT-4; PAPER.md :173/:183, :237; D24)
 // ------------------------------------------------------------------------------------------
+// Quest score mode (score_mode 1, NEXT-1): every page's per-channel min / max key rows live in
+// the page's HBM trailer (after its 16 V rows), maintained by the decode kernel on every write.
+// This kernel (re)builds them from the store over each page's valid rows [0, cnt) -- after
+// prefill and raas_set_state.  Empty pages get +inf / -inf (never read: they are not resident).
+template <int D>
+__global__ void raas_qtrailer_kernel(__nv_bfloat16* kvstore, const int32_t* __restrict__ cnt,
+                                     int units, int C, int pstr) {
+  constexpr int NCH = D / 8;
+  const size_t total = (size_t)units * C * NCH;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % NCH);
+    const size_t pu = i / NCH;
+    const int n = cnt[pu];
+    __nv_bfloat16* kp = kvstore + pu * pstr;
+    uint32_t mn[4] = {0x7f807f80u, 0x7f807f80u, 0x7f807f80u, 0x7f807f80u};
+    uint32_t mx[4] = {0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u};
+    for (int r = 0; r < n; ++r) {
+      const uint4 w = *(reinterpret_cast<const uint4*>(kp + r * D) + (ch ^ (r & 7)));
+      const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        asm("min.bf16x2 %0, %0, %1;" : "+r"(mn[e]) : "r"(wv[e]));
+        asm("max.bf16x2 %0, %0, %1;" : "+r"(mx[e]) : "r"(wv[e]));
+      }
+    }
+    *reinterpret_cast<uint4*>(kp + 2 * PAGE * D + ch * 8) = make_uint4(mn[0], mn[1], mn[2], mn[3]);
+    *reinterpret_cast<uint4*>(kp + 2 * PAGE * D + D + ch * 8) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
+  }
+}
+
 // Representative keys of the full prompt pages: per channel min and max over the 16 keys
 // (exact in bf16), repkey [units][C][2][D].
 template <int D>
 __global__ void raas_repkey_kernel(const __nv_bfloat16* __restrict__ kvstore,
                                    __nv_bfloat16* repkey, const int32_t* __restrict__ nfull,
-                                   int units, int C) {
+                                   int units, int C, int pstr) {
   constexpr int NCH = D / 8;
   const size_t total = (size_t)units * C * NCH;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -365,7 +399,7 @@ __global__ void raas_repkey_kernel(const __nv_bfloat16* __restrict__ kvstore,
     const int pg = (int)(pu % C);
     const size_t u = pu / C;
     if (pg >= nfull[u]) continue;
-    const __nv_bfloat16* kp = kvstore + pu * 2 * PAGE * D;
+    const __nv_bfloat16* kp = kvstore + pu * pstr;
     uint32_t mn[4] = {0x7f807f80u, 0x7f807f80u, 0x7f807f80u, 0x7f807f80u};
     uint32_t mx[4] = {0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u};
 #pragma unroll

@@ -123,3 +123,14 @@ def test_create_rejects_bad_args_without_gpu(L):
     assert b"head_dim" in L.raas_last_error()
     assert L.raas_decode_step(None, None, None, None, None, None) == raas.RAAS_E_INVALID
     assert L.raas_prefill(None, None, None, 0, None) == raas.RAAS_E_INVALID
+
+
+def test_quest_mode_adds_min_max_rows_per_page(L):
+    """score_mode 1 keeps every page's per-channel min / max key rows (Quest's representative
+    keys, PAPER.md :147) in the page's HBM trailer: 2 rows per 32 K/V rows (+6.25 % bytes)."""
+    base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
+    a0 = raas.raas_arena_bytes(raas.make_config(**base))
+    a1 = raas.raas_arena_bytes(raas.make_config(**base, score_mode=1))
+    units, pages = 16, 128
+    trailer = units * pages * 2 * 128 * 2
+    assert trailer <= a1 - a0 <= trailer + 4096

@@ -161,6 +161,29 @@ def test_bitwise_determinism_and_request_sharding():
         assert np.array_equal(np.concatenate([slo[k], shi[k]]), sa[k])
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,L,P,sp,kw", [
+    (1, 32, 8, 1024, 512, 16, {}),                                # config 2 (4 splits per unit)
+    (2, 28, 4, 512, 64, 4, {}),                                   # g = 7, 8 splits per unit
+    (1, 32, 8, 1024, 512, 16, {"score_mode": 1}),                 # generic kernel, Quest scores
+    (2, 8, 2, 256, 40, 8, {"stamp_rule": 1, "top_r": 0.5}),       # generic kernel, top-r
+])
+def test_cluster_schedule_bitwise_equals_default_schedule(monkeypatch, B, Hq, Hkv, L, P, sp, kw):
+    """The cluster schedule (small batches: a unit's split CTAs form a cluster and the leader
+    folds the partials from distributed shared memory) computes exactly what the default
+    schedule (partials through L2) computes: outputs and states bitwise equal."""
+    st = waterfall_stream(71 + Hq + L, B, Hq, Hkv, 128, P, 3 * PAGE * 6)
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("RAAS_CLUSTER", flag)
+        layer = RaasLayer(L, 1e-4, Hq, Hkv, 128, B, split_pages=sp, **kw)
+        runs.append((layer.raas_launch_info(), *_run_gpu(st, L, Hq, Hkv, split_pages=sp, **kw)))
+    (i0, o0, s0), (i1, o1, s1) = runs
+    assert i0["cluster"] == 1 and i1["cluster"] == i1["nsplit"] > 1, (i0, i1)
+    assert i1["grid"] == B * Hkv * i1["nsplit"]
+    assert np.array_equal(o0, o1)
+    assert all(np.array_equal(s0[k], s1[k]) for k in s0)
+
+
 def test_head_sharding_bitwise():
     """Head sharding (SURVEY §8e, config 2's layout): two handles each holding half of the
     kv-heads (and their q-heads) give outputs and states bitwise equal to the unsharded handle's
@@ -551,7 +574,7 @@ def _long_prompt_stream(seed, B, Hq, Hkv, d, P, T):
     (2, 8, 2, 128, 512, 200, 640, 6, 0),     # 32 prompt pages, 6 attended per step
     (2, 28, 4, 128, 256, 160, 384, 4, 8),    # Qwen group, 16 prompt pages
     (1, 4, 2, 64, 160, 120, 256, 3, 0),      # d = 64, 10 prompt pages
-    (2, 8, 2, 128, 200, 120, 320, 4, 0),     # P % 16 = 8: partial last prompt page (always attended)
+    (2, 8, 2, 128, 200, 200, 320, 4, 0),     # P % 16 = 8: partial last prompt page (always attended)
 ])
 def test_quest_prefill_hybrid_lockstep(oracle_mod, B, Hq, Hkv, d, P, T, L, K, sp):
     """quest_prefill_pages = K (PAPER.md :173/:183, :237): GPU vs oracle, bit-exact state and
