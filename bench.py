@@ -416,6 +416,19 @@ def run_ours(args, cfg, rank, world, local_rank):
         for i in range(args.warmup):
             run_step(i % R)
     torch.cuda.synchronize()
+    if args.trace and rank == 0:
+        # CUPTI kernel trace (torch.profiler / Kineto) of 2 model steps of the release build:
+        # per-launch start / end inside the CUDA graphs, i.e. the PDL overlap (evidence only;
+        # the number below is timed without the profiler)
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            with torch.cuda.stream(stream):
+                for i in range(2):
+                    run_step((args.warmup + i) % R)
+            torch.cuda.synchronize()
+        prof.export_chrome_trace(args.trace)
+        log(f"[rank 0] kernel trace of 2 model steps -> {args.trace}")
     if world > 1:
         torch.distributed.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -459,12 +472,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     else:
         occ_mean = float(occ_now)
     nfull = P // 16
+    # Quest score mode: every attended page also brings its min / max key rows (2 of 32 rows:
+    # "+1/16 bytes read"), maintained on write
+    qtr = 4 * d * (occ_mean / 16) if args.score == "quest" and args.page == 16 else 0.0
     if args.quest_prefill and nfull > args.quest_prefill:
         # hybrid: only K of the nfull prompt pages are read, plus their representative keys
         occ_mean -= (nfull - args.quest_prefill) * 16
-        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce + nfull * 4 * d)
+        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce + nfull * 4 * d + qtr)
     else:
-        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce)
+        bytes_launch = units * (4 * d * occ_mean + 4 * d + 4 * g * d + 12 * Ce + qtr)
     variant = bool(args.score != "exact" or args.top_r > 0 or args.table_scope or args.page != 16
                    or args.quest_prefill or args.P or args.L or args.batch or args.layers
                    or args.split_pages or args.dense or heads or mode == "strong")
@@ -684,6 +700,8 @@ def main():
                     help="1: token-level RaaS (PAPER.md §3.2), one timestamp per token (NEXT-3)")
     ap.add_argument("--table-scope", type=int, default=0, choices=[0, 1],
                     help="1: one page table per request, OR over all heads (reading D25)")
+    ap.add_argument("--trace", default="",
+                    help="write a CUPTI kernel trace (chrome json) of 2 model steps before timing")
     ap.add_argument("--dense", type=int, default=0,
                     help="dense comparator: prefill N tokens, L > N + steps (no eviction)")
     args = ap.parse_args()

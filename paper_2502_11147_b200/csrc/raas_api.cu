@@ -365,7 +365,9 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
   for (int G = 1; G <= hi; ++G) {
     const int fu = units / G, R = units - fu * G;
     const long long shared = (long long)R * nsplit;
-    const double cost = (double)fu * nsplit + (double)((shared + G - 1) / G) + (R > 0 ? tail_tiles : 0.0);
+    // units of one split are complete wherever they run (no cross-CTA combine)
+    const double cost = (double)fu * nsplit + (double)((shared + G - 1) / G) +
+                        (R > 0 && nsplit > 1 ? tail_tiles : 0.0);
     if (cost < best_cost - 1e-9 || (cost < best_cost + 1e-9 && G > best)) {
       best_cost = cost;
       best = G;
@@ -375,7 +377,7 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
 }
 
 template <int D, bool TOKD, bool GEN>
-int setup_kernel_t(raas_handle* h) {
+int setup_kernel_t(raas_handle* h, bool want_cl) {
   auto k = decode_kernel<D, TOKD, GEN>();
   h->smem = Lay<D, TOKD, GEN>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
@@ -393,9 +395,7 @@ int setup_kernel_t(raas_handle* h) {
   // (publish + acq_rel counter + loads).  Numerics are the same as the default schedule's.
   h->cl = 0;
   const long long tiles = (long long)h->d.units * h->d.nsplit;
-  bool want = RAAS_CL && !TOKD && h->d.nsplit >= 2 && h->d.nsplit <= 8 && tiles <= h->num_sms * per_sm;
-  if (const char* e = std::getenv("RAAS_CLUSTER")) want = want && std::atoi(e) != 0;  // A/B only
-  if (want) {
+  if (want_cl && GEN && !TOKD) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3((unsigned)tiles);
     lc.blockDim = dim3(Lay<D, TOKD, GEN>::THREADS);
@@ -419,8 +419,21 @@ int setup_kernel_t(raas_handle* h) {
 }
 template <int D>
 int setup_kernel(raas_handle* h) {
-  return h->d.tokd ? setup_kernel_t<D, true, false>(h)
-                   : h->d.gen ? setup_kernel_t<D, false, true>(h) : setup_kernel_t<D, false, false>(h);
+  if (h->d.tokd) return setup_kernel_t<D, true, false>(h, false);
+  // cluster schedule (generic instantiation) when the (unit, split) tiles fit the SMs one per
+  // CTA and every unit is split; RAAS_CLUSTER=0 disables it (A/B experiments, tests)
+  const long long tiles = (long long)h->d.units * h->d.nsplit;
+  bool want_cl = RAAS_CL && h->d.nsplit >= 2 && h->d.nsplit <= 8 && tiles <= h->num_sms;
+  if (const char* e = std::getenv("RAAS_CLUSTER")) want_cl = want_cl && std::atoi(e) != 0;
+  if (h->d.gen || want_cl) {
+    int rc = setup_kernel_t<D, false, true>(h, want_cl);
+    if (rc || h->d.gen) return rc;
+    if (h->cl) {
+      h->d.gen = 1;  // launch the generic instantiation (it carries the cluster schedule)
+      return RAAS_OK;
+    }
+  }
+  return setup_kernel_t<D, false, false>(h, false);
 }
 
 int build_repkeys(raas_handle* h, cudaStream_t st) {

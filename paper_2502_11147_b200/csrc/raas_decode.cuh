@@ -122,7 +122,9 @@ struct TileSched {
       owned = true;
       return b * n_owned + i_owned++;
     }
-    owned = false;
+    // a grabbed tile of a one-split unit is the whole unit: it takes the owned path (out and
+    // LSE from the merge warp, no partial through L2), whichever CTA grabs it
+    owned = nsplit == 1;
     if (n_shared_tiles == 0) return -1;
     int x = 0;
     if (lane == 0) x = atomicAdd(grab, 1);
@@ -726,7 +728,10 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
   auto cqfull = [&](int q) { return bar + 8 * (2 * S + 6 + q); };
   auto cqempty = [&](int q) { return bar + 8 * (2 * S + 6 + CQ + q); };
   const uint32_t clfull = bar + 8 * (2 * S + 6 + 2 * CQ);  // cluster schedule: partials published
-  const bool cl = RAAS_CL && !TOKD && p.cl != 0;
+  // the cluster schedule lives in the generic instantiation only: small batches are latency
+  // bound, and keeping it out of the lean kernel keeps that kernel's registers (and the
+  // host-buffer path's co-resident ingest kernel) where they were
+  const bool cl = RAAS_CL && GEN && !TOKD && p.cl != 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef RAAS_DBG_TIMING
@@ -926,7 +931,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
       owned = owned_next;
       const int p0 = split * SP;
       const int n = min(p0 + SP, natt) - p0;
-      if (n <= 0) continue;  // pages not yet allocated (fill phase)
+      if (n <= 0) {  // pages not yet allocated (fill phase)
+        // cluster schedule: the leader expects an arrival from every CTA of the cluster; an
+        // empty split publishes nothing (its combine folds only the nse non-empty splits)
+        if (cl) mbar_arrive_remote(mapa(clfull, 0));
+        continue;
+      }
       const int slot = pl.x, off = pl.y & 0xffff;
       // align the tile to the consumer count: page i of a tile is always consumed by warp
       // i % NC, so the split's arithmetic does not depend on the schedule (determinism)

@@ -20,6 +20,13 @@ METRICS = [
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "launch__shared_mem_per_block_dynamic", "sm__inst_executed_pipe_tensor.sum",
     "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    # SURVEY §8(d)'s list: tensor pipe (confirms the MMAs), long-scoreboard share, achieved
+    # occupancy (= sm__warps_active.avg.pct_of_peak_sustained_active)
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "sm__maximum_warps_per_active_cycle_pct",
 ]
 
 

@@ -15,8 +15,13 @@ r3, _, _ = run_lockstep(oracle, st, L=256, alpha=1e-4, Hq=8, Hkv=2, split_pages=
 st = waterfall_stream(9, 2, 8, 2, 128, 37, 60)
 r4, _, _ = run_lockstep(oracle, st, L=96, alpha=1e-3, Hq=8, Hkv=2, split_pages=2, page=1, state_every=4)
 r5, _, _ = run_lockstep(oracle, st, L=96, alpha=1e-3, Hq=8, Hkv=2, split_pages=2, page=1, table_scope=1)
-print("sanitize case ok", r1.max_err, r2.max_err, r3.max_err, r4.max_err, r5.max_err,
-      r1.band_events + r2.band_events + r3.band_events + r4.band_events + r5.band_events)
+# cluster schedule (B = 1: each unit's 4 split CTAs exchange partials through distributed
+# shared memory), from the prompt on, so the fill phase's empty splits are exercised
+st = waterfall_stream(10, 1, 32, 8, 128, 100, 90)
+r6, ly6, _ = run_lockstep(oracle, st, L=512, alpha=1e-4, Hq=32, Hkv=8, split_pages=8)
+assert ly6.raas_launch_info()["cluster"] == 4
+print("sanitize case ok", r1.max_err, r2.max_err, r3.max_err, r4.max_err, r5.max_err, r6.max_err,
+      r1.band_events + r2.band_events + r3.band_events + r4.band_events + r5.band_events + r6.band_events)
 
 # early start (two handles interleaved on one stream) and the zero-copy host path
 import numpy as np, torch
