@@ -55,6 +55,8 @@ using Lay = raas::DecodeLayout<D, NC, S, TOKD, GEN>;
 // deferred token level (tokd)
 template <int D, bool TOKD, bool GEN>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD, GEN>; }
+template <int D>
+constexpr auto decode_kernel_cl() { return raas::raas_decode_kernel<D, NC, S, false, false, true>; }
 
 struct Layout {
   size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, req_x, req_ctr,
@@ -345,6 +347,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   lc.numAttrs = h->cl ? 2 : 1;
   if (h->d.tokd)     RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true, false>(), p));
   else if (h->d.gen) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, true>(), p));
+  else if (h->cl)    RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_cl<D>(), p));
   else               RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, false>(), p));
   return RAAS_OK;
 }
@@ -378,7 +381,7 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
 
 template <int D, bool TOKD, bool GEN>
 int setup_kernel_t(raas_handle* h, bool want_cl) {
-  auto k = decode_kernel<D, TOKD, GEN>();
+  auto k = want_cl ? decode_kernel_cl<D>() : decode_kernel<D, TOKD, GEN>();
   h->smem = Lay<D, TOKD, GEN>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
@@ -395,7 +398,7 @@ int setup_kernel_t(raas_handle* h, bool want_cl) {
   // (publish + acq_rel counter + loads).  Numerics are the same as the default schedule's.
   h->cl = 0;
   const long long tiles = (long long)h->d.units * h->d.nsplit;
-  if (want_cl && GEN && !TOKD) {
+  if (want_cl && !GEN && !TOKD) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3((unsigned)tiles);
     lc.blockDim = dim3(Lay<D, TOKD, GEN>::THREADS);
@@ -420,18 +423,17 @@ int setup_kernel_t(raas_handle* h, bool want_cl) {
 template <int D>
 int setup_kernel(raas_handle* h) {
   if (h->d.tokd) return setup_kernel_t<D, true, false>(h, false);
+  if (std::getenv("RAAS_FORCE_GEN")) h->d.gen = 1;  // A/B experiments: the generic instantiation
   // cluster schedule (generic instantiation) when the (unit, split) tiles fit the SMs one per
   // CTA and every unit is split; RAAS_CLUSTER=0 disables it (A/B experiments, tests)
   const long long tiles = (long long)h->d.units * h->d.nsplit;
-  bool want_cl = RAAS_CL && h->d.nsplit >= 2 && h->d.nsplit <= 8 && tiles <= h->num_sms;
+  bool want_cl = RAAS_CL && Lay<D>::CL_OK && !h->d.gen && h->d.nsplit >= 2 && h->d.nsplit <= 8 &&
+                 tiles <= h->num_sms;
   if (const char* e = std::getenv("RAAS_CLUSTER")) want_cl = want_cl && std::atoi(e) != 0;
-  if (h->d.gen || want_cl) {
-    int rc = setup_kernel_t<D, false, true>(h, want_cl);
-    if (rc || h->d.gen) return rc;
-    if (h->cl) {
-      h->d.gen = 1;  // launch the generic instantiation (it carries the cluster schedule)
-      return RAAS_OK;
-    }
+  if (h->d.gen) return setup_kernel_t<D, false, true>(h, false);
+  if (want_cl) {
+    int rc = setup_kernel_t<D, false, false>(h, true);
+    if (rc || h->cl) return rc;  // else clusters of this size do not fit: default schedule
   }
   return setup_kernel_t<D, false, false>(h, false);
 }

@@ -177,6 +177,11 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
@@ -229,7 +234,11 @@ struct DecodeLayout {
   // cluster schedule (p.cl): the tile's split partial, published in this CTA's merge area once
   // the merge warp has read the (only) tile's deposits: float2 (m, l)[MAX_GROUP], then
   // float acc[g][D]; read by the cluster's leader through distributed shared memory
-  static_assert(PUB_ACC_OFF + MAX_GROUP * D * 4 <= NDEP * NC * DEPOSIT, "publish area");
+  // cluster schedule (p.cl): the leader receives split s's partial at OFF_RECV + s * RECV_SLOT,
+  // the second half of the deposit area (each CTA streams one tile: only deposit parity 0 is used)
+  static constexpr int RECV_SLOT = PUB_ACC_OFF + MAX_GROUP * D * 4;
+  static constexpr int OFF_RECV = OFF_MERGE + NC * DEPOSIT;
+  static constexpr bool CL_OK = NDEP == 2 && 8 * RECV_SLOT <= NC * DEPOSIT;
   static constexpr int BYTES = OFF_BAR + NBAR * 8;
   static constexpr int SMEM = BYTES + 1024;  // + alignment slack
   static constexpr int THREADS = (NC + 3) * 32;  // producer, merge, combine, NC consumers
@@ -242,10 +251,11 @@ template <int D, bool GEN>
 __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, int nse, uint32_t scr,
                                              int lane, bool outdone, bool CL = false, uint32_t pub = 0,
                                              uint32_t clbar = 0) {
-  // CL (cluster schedule): split s's partial is in the merge area of the cluster's CTA s
-  // (`pub`, read through distributed shared memory) once every CTA's merge warp has arrived
-  // on the leader's `clbar` (release / acquire at cluster scope); the arithmetic below is the
-  // same as for partials read from L2, so results do not depend on the schedule
+  // CL (cluster schedule): the cluster's CTA s stored split s's partial into this (leader) CTA's
+  // receive area `pub` (slot s, distributed shared memory stores) before arriving on `clbar`
+  // (release / acquire at cluster scope); the arithmetic below is the same as for partials
+  // read from L2, so results do not depend on the schedule
+  constexpr int RSLOT = PUB_ACC_OFF + MAX_GROUP * D * 4;
   if (CL) mbar_wait_cluster(clbar, 0);
   // outdone: the merge warp already folded the splits and wrote out; the LSE is in scr_lse
   // GEN = false: the default method (page = 16, alpha rule, one table per kv-head) with the
@@ -268,7 +278,9 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   for (int k = 0; k < 2; ++k) {
     const int i = 32 * k + lane;
     mla[k] = (outdone || i >= NE) ? make_float2(-INFINITY, 0.f)
-             : CL ? ld_dsmem_f32x2(mapa(pub + 8 * (i % g), i / g)) : __ldcg(ml_g + i);
+             : CL ? make_float2(lds_f32(pub + (i / g) * RSLOT + 8 * (i % g)),
+                                lds_f32(pub + (i / g) * RSLOT + 8 * (i % g) + 4))
+                  : __ldcg(ml_g + i);
   }
   // page metadata for a6/a7 (bounded by C, masked by the plan's page count later)
   constexpr int PPL = 4;  // pages per lane per chunk
@@ -313,7 +325,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       for (int u = 0; u < SG; ++u) {
         const bool ok = !outdone && c < nch && s0 + u < nse;
         v[i][u] = !ok ? make_float4(0.f, 0.f, 0.f, 0.f)
-                  : CL ? ld_dsmem_f32x4(mapa(pub + PUB_ACC_OFF + (h * D + 4 * d4) * 4, s0 + u))
+                  : CL ? lds_f32x4(pub + (s0 + u) * RSLOT + PUB_ACC_OFF + (h * D + 4 * d4) * 4)
                        : __ldcg(reinterpret_cast<const float4*>(acc_g + ((size_t)(s0 + u) * g + h) * D) + d4);
       }
     }
@@ -327,7 +339,9 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       if (i < NE) { sts_f32(scr_w + 8 * i, mla[k].x); sts_f32(scr_w + 8 * i + 4, mla[k].y); }
     }
     for (int i = 64 + lane; i < NE; i += 32) {  // more than 64 (split, head) pairs
-      const float2 ml = CL ? ld_dsmem_f32x2(mapa(pub + 8 * (i % g), i / g)) : __ldcg(ml_g + i);
+      const float2 ml = CL ? make_float2(lds_f32(pub + (i / g) * RSLOT + 8 * (i % g)),
+                                         lds_f32(pub + (i / g) * RSLOT + 8 * (i % g) + 4))
+                           : __ldcg(ml_g + i);
       sts_f32(scr_w + 8 * i, ml.x);
       sts_f32(scr_w + 8 * i + 4, ml.y);
     }
@@ -693,9 +707,11 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 #ifdef RAAS_DBG_TOKD_GLOBAL
 __device__ int g_tokd_dbg[16];
 #endif
-template <int D, int NC, int S, bool TOKD, bool GEN>
+template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false>
 __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
+  // CL: the cluster-schedule instantiation of the default method (small batches); the other
+  // instantiations carry none of its code (registers: see DESIGN.md §6)
   // GEN = false (and !TOKD): the default method only (page = 16, exact page score, alpha rule,
   // per-kv-head tables, no Quest-on-prefill); the options' run-time branches are compiled out
   const int quest_k = GEN ? p.quest_k : 0;
@@ -728,10 +744,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
   auto cqfull = [&](int q) { return bar + 8 * (2 * S + 6 + q); };
   auto cqempty = [&](int q) { return bar + 8 * (2 * S + 6 + CQ + q); };
   const uint32_t clfull = bar + 8 * (2 * S + 6 + 2 * CQ);  // cluster schedule: partials published
-  // the cluster schedule lives in the generic instantiation only: small batches are latency
-  // bound, and keeping it out of the lean kernel keeps that kernel's registers (and the
-  // host-buffer path's co-resident ingest kernel) where they were
-  const bool cl = RAAS_CL && GEN && !TOKD && p.cl != 0;
+  const bool cl = RAAS_CL && Lay::CL_OK && CL && !TOKD && p.cl != 0;
+  const uint32_t recv = base + Lay::OFF_RECV;  // cluster schedule: the splits' partials (leader)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef RAAS_DBG_TIMING
@@ -826,7 +840,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
       if constexpr (TOKD) combine_unit_tok<D>(p, unit, nse_u, scratch, lane);
-      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane, outdone, cl, merge, clfull);
+      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane, outdone, cl, recv, clfull);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -1121,21 +1135,28 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
         continue;
       }
       if (cl) {
-        // cluster schedule: the partial goes to this CTA's merge area (its deposits are read:
-        // the tile was the CTA's only one), then every lane arrives on the leader's barrier;
-        // the leader's combine reads all splits' partials through distributed shared memory
+        // cluster schedule: this split's partial goes straight into the leader's receive slot
+        // (distributed shared memory stores), then every lane arrives on the leader's barrier
+        // (release at cluster scope orders its stores before the leader's acquire)
+        const uint32_t slot = mapa(recv + split * Lay::RECV_SLOT, 0);
         if (lane < 4) {
-          if (2 * qd < g) sts_f32(merge + 8 * (2 * qd), M0), sts_f32(merge + 8 * (2 * qd) + 4, L0);
-          if (2 * qd + 1 < g) sts_f32(merge + 8 * (2 * qd + 1), M1), sts_f32(merge + 8 * (2 * qd + 1) + 4, L1);
+          if (2 * qd < g) {
+            st_dsmem_f32(slot + 8 * (2 * qd), M0);
+            st_dsmem_f32(slot + 8 * (2 * qd) + 4, L0);
+          }
+          if (2 * qd + 1 < g) {
+            st_dsmem_f32(slot + 8 * (2 * qd + 1), M1);
+            st_dsmem_f32(slot + 8 * (2 * qd + 1) + 4, L1);
+          }
         }
-        const uint32_t pa0 = merge + PUB_ACC_OFF + ((2 * qd) * D + r) * 4, pa1 = pa0 + D * 4;
+        const uint32_t pa0 = slot + PUB_ACC_OFF + ((2 * qd) * D + r) * 4, pa1 = pa0 + D * 4;
 #pragma unroll
         for (int mt = 0; mt < KS; ++mt) {
-          if (2 * qd < g) { sts_f32(pa0 + 64 * mt, acc[4 * mt + 0]); sts_f32(pa0 + 64 * mt + 32, acc[4 * mt + 2]); }
-          if (2 * qd + 1 < g) { sts_f32(pa1 + 64 * mt, acc[4 * mt + 1]); sts_f32(pa1 + 64 * mt + 32, acc[4 * mt + 3]); }
+          if (2 * qd < g) { st_dsmem_f32(pa0 + 64 * mt, acc[4 * mt + 0]); st_dsmem_f32(pa0 + 64 * mt + 32, acc[4 * mt + 2]); }
+          if (2 * qd + 1 < g) { st_dsmem_f32(pa1 + 64 * mt, acc[4 * mt + 1]); st_dsmem_f32(pa1 + 64 * mt + 32, acc[4 * mt + 3]); }
         }
         mbar_arrive_remote(mapa(clfull, 0));
-        if (cluster_ctarank() == 0) push(unit | nse << CQ_UNIT_BITS);
+        if (split == 0) push(unit | nse << CQ_UNIT_BITS);  // split 0 is the leader's (rank 0)
         continue;
       }
       // publish the tile's split-K partial (m, l, acc) in the C-fragment layout
