@@ -229,17 +229,18 @@ def cpu_count_info():
     return n, model
 
 
-def oracle_sample(cfg, seconds=12.0, max_steps=100000, seed=4242):
+def oracle_sample(cfg, seconds=12.0, max_steps=100000, seed=4242, threads=0):
     """Time the fp64 CPU oracle (as it stands) on a bounded sample of the workload: one layer,
     `threads` units of the config from a full-cache state, steady-state decode steps until
-    `seconds` elapse.  Returns unit-steps/s and a description."""
+    `seconds` elapse.  threads = 0: every host core.  Returns unit-steps/s, the threads used and
+    a description."""
     import numpy as np
 
     import oracle
     from paper_2502_11147_b200.synth import bf16_bits, random_steady_state
 
-    threads, cpu_model = cpu_count_info()
-    threads = oracle.set_threads(threads)
+    ncores, cpu_model = cpu_count_info()
+    threads = oracle.set_threads(threads if threads > 0 else ncores)
     g = cfg["hq"] // cfg["hkv"]
     C, Pp = cfg["L"] // 16, -(-cfg["P"] // 16)
     n_units = max(cfg["hkv"], (threads // cfg["hkv"]) * cfg["hkv"])
@@ -550,8 +551,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         ups, threads, desc = oracle_sample(cfg, seconds=args.cpu_seconds)
+        ups1, _, desc1 = oracle_sample(cfg, seconds=max(2.0, args.cpu_seconds / 4), threads=1)
         cpu = {"value": ups / (units * nl), "unit": UNIT, "cores": threads,
-               "kind": "oracle", "sample": desc, "unit_steps_per_s": ups}
+               "kind": "oracle", "sample": desc, "unit_steps_per_s": ups,
+               "single_thread": {"value": ups1 / (units * nl), "unit": UNIT, "cores": 1,
+                                 "unit_steps_per_s": ups1, "sample": desc1}}
     l2_note = (f"{nl * rot} distinct layer caches ({rot} rotation(s) of {nl}) = "
                f"{cache_bytes / 2**30:.3f} GiB vs L2 {l2 / 2**20:.0f} MiB: "
                + (f">= 4x L2, consecutive steps read disjoint caches (no flush needed)"

@@ -74,7 +74,8 @@ def test_arena_bytes(L, cfg, expect):
                                    dict(quest_prefill_pages=8, L=16384), dict(table_scope=2),
                                    dict(page=8), dict(page=1, L=2040), dict(page=1, score_mode=1),
                                    dict(page=1, quest_prefill_pages=4),
-                                   dict(page=1, stamp_rule=1, L=1024), dict(disable_early_start=2)])
+                                   dict(page=1, stamp_rule=1, L=1024), dict(disable_early_start=2),
+                                   dict(L=80 * 32 * 16 + 16)])   # > MAX_SPLITS x 32-page splits
 def test_arena_bytes_rejects_bad_modes(L, extra):
     base = dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=2)
     base.update(extra)

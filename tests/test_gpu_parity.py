@@ -363,6 +363,33 @@ def test_full_size_sampled_units_lockstep(oracle_mod, cfg, B, Hq, Hkv, L, P, sp,
     assert layer.raas_get_status() == 0
 
 
+def test_max_budget_lockstep(oracle_mod):
+    """The largest budget one handle supports at the default split size: L = 80 splits x 32
+    pages x 16 = 40960 tokens (MAX_SPLITS partials per unit), from a full-cache waterfall state
+    with a partial current page, g = 8 (the largest GQA group), 40 steps in lockstep."""
+    B, Hq, Hkv, d, L, P, T = 1, 8, 1, 128, 40960, 128, 40
+    state, kst, vst, steps = waterfall_resume(99, B, Hq, Hkv, d, L, P, T, cur_count=7, lam=6.0,
+                                              span=1)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    assert layer.raas_launch_info()["nsplit"] == 80
+    layer.raas_set_state(state["t"], state["ts"], state["start"], state["count"], state["pinned"],
+                         kst, vst)
+    orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
+                            batch=B)
+    orc.set_state(state["t"], state["ts"], state["start"], state["count"], state["pinned"], kst, vst)
+    res = LockstepResult()
+    out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
+    for i in range(T):
+        layer.raas_decode_step(to_dev(steps.q[i]), to_dev(steps.k[i]), to_dev(steps.v[i]), out)
+        o_out = orc.decode_step(steps.q[i], steps.k[i], steps.v[i])
+        res.max_err = max(res.max_err, float(np.abs(bf16_to_f32(from_dev(out)) - o_out).max()))
+        tr = orc.get_trace()
+        res.evictions += int((tr["evicted"] >= 0).sum())
+        compare_sampled(layer, orc, [0], 1e-4, tr["pstar"], res)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL and res.evictions >= 2
+    assert layer.raas_get_status() == 0
+
+
 def test_bench_waterfall_stream_lockstep(oracle_mod):
     """The exact stream bench.py times at config 3 (WaterfallTorch drawn on the GPU, lambda = 7,
     seed 1000 * 3 + rank 0): prefill, the bench's fill to steady state ((C - Pp) * 16 + 256
