@@ -25,6 +25,9 @@
 //                  the <= 8 q-heads of the GQA group = N), online softmax in fp32 registers.
 #pragma once
 
+#ifndef RAAS_MINB
+#define RAAS_MINB 1  // resident CTAs per SM the kernel is compiled for (register budget)
+#endif
 #ifndef RAAS_CL
 #define RAAS_CL 1  // compile the cluster schedule (DecodeParams::cl) into the kernels
 #endif
@@ -708,7 +711,7 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 __device__ int g_tokd_dbg[16];
 #endif
 template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false>
-__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, 1)
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RAAS_MINB)
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
   // CL: the cluster-schedule instantiation of the default method (small batches); the other
   // instantiations carry none of its code (registers: see DESIGN.md §6)
