@@ -50,6 +50,26 @@ def test_sass_is_sm100a_and_uses_bulk_copies_and_tensor_cores(L):
     assert "LDSM" in sass and "MOVM" in sass
 
 
+def test_sass_cluster_instantiation_uses_cluster_barriers(L):
+    """The small-batch cluster schedule's kernel (raas_decode_kernel<..., CL = true>) carries the
+    thread-block-cluster barrier (barrier.cluster -> UCGABAR) and remote mbarrier arrivals on the
+    leader (mbarrier.arrive.release.cluster -> SYNCS.ARRIVE...RED); the default lean kernel
+    carries none of it."""
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump) and not shutil.which("cuobjdump"):
+        pytest.skip("no cuobjdump")
+    import subprocess
+
+    def sass(fn):
+        return subprocess.run([cuobjdump, "-sass", "-fun", fn, raas.LIB_PATH], capture_output=True,
+                              text=True).stdout
+    cl = sass("_ZN4raas18raas_decode_kernelILi128ELi8ELi16ELb0ELb0ELb1EEEvNS_12DecodeParamsE")
+    lean = sass("_ZN4raas18raas_decode_kernelILi128ELi8ELi16ELb0ELb0ELb0EEEvNS_12DecodeParamsE")
+    assert "UCGABAR_ARV" in cl and "UCGABAR_WAIT" in cl and "SYNCS.ARRIVE.TRANS64.RED" in cl
+    assert "HMMA.16816.F32.BF16" in cl and "UBLKCP" in cl
+    assert lean and "UCGABAR" not in lean
+
+
 @pytest.mark.parametrize("cfg,expect", [
     (dict(L=64, alpha=1e-4, n_q_heads=4, n_kv_heads=2, head_dim=64, batch=1), True),
     (dict(L=2048, alpha=1e-4, n_q_heads=32, n_kv_heads=8, head_dim=128, batch=64), True),
