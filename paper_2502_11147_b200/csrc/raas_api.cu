@@ -427,8 +427,12 @@ int setup_kernel(raas_handle* h) {
   // cluster schedule (generic instantiation) when the (unit, split) tiles fit the SMs one per
   // CTA and every unit is split; RAAS_CLUSTER=0 disables it (A/B experiments, tests)
   const long long tiles = (long long)h->d.units * h->d.nsplit;
+  // the leader's receive area holds nsplit partials and the unit's page maxima [C][g] fp32,
+  // and its combine's preloaded metadata covers C <= 32 * CLM pages
+  const long long recv_need = (long long)h->d.nsplit * Lay<D>::RECV_SLOT + 4LL * h->d.C * h->d.g;
   bool want_cl = RAAS_CL && Lay<D>::CL_OK && !h->d.gen && h->d.nsplit >= 2 && h->d.nsplit <= 8 &&
-                 tiles <= h->num_sms;
+                 tiles <= h->num_sms && recv_need <= (long long)NC * Lay<D>::DEPOSIT &&
+                 h->d.C <= 32 * raas::CLM;
   if (const char* e = std::getenv("RAAS_CLUSTER")) want_cl = want_cl && std::atoi(e) != 0;
   if (h->d.gen) return setup_kernel_t<D, false, true>(h, false);
   if (want_cl) {

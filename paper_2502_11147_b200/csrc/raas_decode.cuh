@@ -546,6 +546,117 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
 
 
 // ---------------------------------------------------------------------------------------------
+// Cluster schedule (small batches, the default method): a5-a7 for the cluster's unit by the
+// leader's combine warp with no L2 round trip on its critical path.  The unit's plan, pinned
+// count and per-page (ts, start) were loaded at kernel start (`cm`: they are the previous step's
+// state); the splits' (m, l, acc) partials and the page maxima arrive in this CTA's shared
+// memory from the cluster's merge warps / consumers (`recv`, `pmx`).  Every operation and its
+// order are those of combine_unit (split-order running merge, strict threshold, (ts, start)
+// argmin), so results are bitwise those of the default schedule.
+// ---------------------------------------------------------------------------------------------
+constexpr int CLM = 8;  // pages per lane the preloaded metadata covers (C <= 256)
+struct ClMeta {
+  int4 pl;
+  int npin;
+  int ts[CLM], st[CLM];
+};
+template <int D>
+__device__ __forceinline__ void combine_unit_cl(const DecodeParams& p, int unit, int nse, uint32_t scr,
+                                                int lane, uint32_t recv, uint32_t pmx,
+                                                uint32_t clbar, const ClMeta& cm) {
+  constexpr int RSLOT = PUB_ACC_OFF + MAX_GROUP * D * 4;
+  const int C = p.C, g = p.g;
+  const uint32_t scr_w = scr;                                   // float2[nse][g] split factors
+  const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
+  const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
+  mbar_wait_cluster(clbar, 0);  // every split's partial and page maxima are here
+  // ---- a5 (1): running merge of the split statistics -> factors, LSE, 1 / l ----
+  if (lane < g) {
+    float m = -INFINITY, l = 0.f;
+    for (int s = 0; s < nse; ++s) {
+      const uint32_t a = recv + s * RSLOT + 8 * lane;
+      float mn, fa, fb;
+      merge_factors(m, lds_f32(a), mn, fa, fb);
+      l = fmaf(l, fa, __fmul_rn(lds_f32(a + 4), fb));
+      m = mn;
+      sts_f32(scr_w + 8 * (s * g + lane), fa);
+      sts_f32(scr_w + 8 * (s * g + lane) + 4, fb);
+    }
+    sts_f32(scr_lse + 4 * lane, m + log2f(l));
+    sts_f32(scr_inv + 4 * lane, 1.f / l);
+  }
+  __syncwarp();
+  // ---- a5 (2): out[h][d] = acc[h][d] / l_h, acc folded in split order ----
+  constexpr int CPH = D / 4;
+  const int nch = g * CPH;
+  for (int c = lane; c < nch; c += 32) {
+    const int h = c / CPH, d4 = c - h * CPH;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < nse; ++s) {
+      const float4 v = lds_f32x4(recv + s * RSLOT + PUB_ACC_OFF + (h * D + 4 * d4) * 4);
+      const float fa = lds_f32(scr_w + 8 * (s * g + h)), fb = lds_f32(scr_w + 8 * (s * g + h) + 4);
+      o.x = fmaf(o.x, fa, __fmul_rn(v.x, fb));
+      o.y = fmaf(o.y, fa, __fmul_rn(v.y, fb));
+      o.z = fmaf(o.z, fa, __fmul_rn(v.z, fb));
+      o.w = fmaf(o.w, fa, __fmul_rn(v.w, fb));
+    }
+    const float inv = lds_f32(scr_inv + 4 * h);
+    *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) =
+        make_uint2(pack_bf16x2(o.x * inv, o.y * inv), pack_bf16x2(o.z * inv, o.w * inv));
+  }
+  // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
+  float lse[MAX_GROUP];
+#pragma unroll
+  for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
+  const int4 pl = cm.pl;
+  const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
+  const int used_eff = pl.z, t = pl.w, npin = cm.npin;
+  Cand best{~0ull, -1};
+  int n_stamp = 0, n_dec = 0;
+#pragma unroll
+  for (int i = 0; i < CLM; ++i) {
+    const int pg = 32 * i + lane;
+    if (pg < used_eff) {
+      int ts_p = cm.ts[i], st_p = cm.st[i];
+      const bool is_slot = pg == slot;
+      const size_t ix = (size_t)unit * C + pg;
+      if (is_slot) {
+        if (off == 0) {
+          st_p = t;
+          p.start[ix] = t;
+        }
+        p.cnt[ix] = off + 1;
+      }
+      if (pg >= npin) {
+        float x = -INFINITY;
+#pragma unroll
+        for (int h = 0; h < MAX_GROUP; ++h)
+          if (h < g) x = fmaxf(x, lds_f32(pmx + 4 * (pg * g + h)) - lse[h]);
+        const bool stamp = x > p.log2_alpha;  // strict (D3)
+        ++n_dec;
+        n_stamp += stamp ? 1 : 0;
+        if (stamp || is_slot) {  // stamp, or write refresh (D8)
+          ts_p = t;
+          p.ts[ix] = t;
+        }
+        cand_update(best, cand_key(ts_p, st_p), pg);
+      }
+    }
+  }
+  const int victim = warp_argmin_page(best);
+  n_stamp = warp_sum_i(n_stamp);
+  n_dec = warp_sum_i(n_dec);
+  if (lane == 0) {
+    p.plan[unit] = next_plan(slot, off + 1, used_eff, C, t, victim, p.status, PAGE);
+    atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
+    atomicAdd(p.stats + 1, (unsigned long long)n_dec);
+    p.counter[unit] = 0;
+    if (evicting) atomicAdd(p.stats + 2, 1ull);
+    atomicAdd(p.stats + 3, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Deferred token-level combine (tokd; NEXT-3): the pass attended the resident rows [0, used)
 // and took step t-1's stamp decisions.  Here: victim = min over the splits' candidates (if the
 // cache is full), out = softmax over (resident - victim + new token), LSE_t and q_t stored for
@@ -1189,7 +1300,37 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
     dbg_add(9, t_start);
   } else if (warp == 2) {
     // ============================ combine (per unit) ============================
-    combine_loop(scr);
+    if (cl) {
+      // cluster schedule: only the leader combines, one unit, with its metadata loaded now (the
+      // previous step's state, final once griddepcontrol.wait returned above) so none of its
+      // loads sits on the combine's critical path
+      if (cluster_ctarank() == 0) {
+        const int unit = blockIdx.x / p.nsplit;
+        ClMeta cm;
+        cm.pl = __ldcg(p.plan + unit);
+        cm.npin = __ldg(p.npin + unit);
+#pragma unroll
+        for (int i = 0; i < CLM; ++i) {
+          const int pg = 32 * i + lane;
+          cm.ts[i] = pg < C ? __ldcg(p.ts + (size_t)unit * C + pg) : 0;
+          cm.st[i] = pg < C ? __ldcg(p.start + (size_t)unit * C + pg) : 0;
+        }
+        int i = 0;
+        if (lane == 0) i = atomicAdd(pop_ctr, 1);  // index 0: the unit (the consumers never pop)
+        i = __shfl_sync(0xffffffffu, i, 0);
+        mbar_wait(cqfull(i % CQ), (i / CQ) & 1);
+        int entry = 0;
+        if (lane == 0) entry = cq[i % CQ];
+        entry = __shfl_sync(0xffffffffu, entry, 0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(cqempty(i % CQ));
+        if (entry >= 0)
+          combine_unit_cl<D>(p, entry & ((1 << CQ_UNIT_BITS) - 1), (entry >> CQ_UNIT_BITS) & CQ_NSE_MASK,
+                             scr, lane, recv, recv + p.nsplit * Lay::RECV_SLOT, clfull, cm);
+      }
+    } else {
+      combine_loop(scr);
+    }
     dbg_add(10, t_start);
 #ifdef RAAS_DBG_TIMING
     if (lane == 0) g_raas_dbg[blockIdx.x][14] = dbg_gtimer();
@@ -1227,7 +1368,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
             atomicAdd(p.stats + 1, (unsigned long long)n_dec);
           }
         }
-        if constexpr (Lay::JOIN) combine_loop(ring + s * STAGE);  // join the tail's combines
+        if constexpr (Lay::JOIN) {
+          if (!cl) combine_loop(ring + s * STAGE);  // join the tail's combines
+        }
         break;
       }
       if (flags & FLAG_SKIP) {
@@ -1527,6 +1670,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
         if (!TOKD && r + 8 < cnt) {
           if (2 * qd < g) px[8 * g + 2 * qd] = s2;
           if (2 * qd + 1 < g) px[8 * g + 2 * qd + 1] = s3;
+        }
+      } else if (cl) {  // cluster schedule: the page maxima go to the leader's shared memory
+        if (lane < 4) {
+          const uint32_t pa = mapa(recv + p.nsplit * Lay::RECV_SLOT + 4 * (page * g), 0);
+          if (2 * qd < g) st_dsmem_f32(pa + 4 * (2 * qd), sc0);
+          if (2 * qd + 1 < g) st_dsmem_f32(pa + 4 * (2 * qd + 1), sc1);
         }
       } else if (lane < 4) {  // a4: page score per head ("a single attention score per page", :147)
         float* pmx = p.pmax + (size_t)(unit * C + page) * g;
