@@ -28,6 +28,9 @@
 #ifndef RAAS_MINB
 #define RAAS_MINB 1  // resident CTAs per SM the kernel is compiled for (register budget)
 #endif
+#ifndef RAAS_PRE
+#define RAAS_PRE 0  // pages issued before griddepcontrol.wait (early start); 0: see the producer
+#endif
 #ifndef RAAS_CL
 #define RAAS_CL 1  // compile the cluster schedule (DecodeParams::cl) into the kernels
 #endif
@@ -1040,7 +1043,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
         const int unit = tile / p.nsplit, p0 = (tile - unit * p.nsplit) * SP;
         const int n = min(p0 + SP, nnatt) - p0;
         if (n > 0) {
-          pre = min(n, BATCH);
+          // the whole first tile when the ring holds it (16-page tiles: small budgets, B = 1;
+          // -1 % there), else one batch (32-page tiles: a second batch early cost config 4 +0.6 %)
+          pre = RAAS_PRE > 0 ? min(n, RAAS_PRE < S ? RAAS_PRE : S) : (n <= S ? n : min(n, BATCH));
           issue_batch(0, pre, 0, unit, n, 0, ncnt, nphys, nplan.x, nplan.y & 0xffff);
         }
       }

@@ -1,2 +1,2 @@
-for rep in 1 2; do for sp in 16 8 4; do timeout 300 python bench.py --config 2 --steps 200 --split-pages $sp --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('sp=$sp', round(d['roofline']['avg_launch_us'],2), 'us', d['launch'])"; done; done
-for B in 2 4; do timeout 300 python bench.py --config 2 --batch $B --steps 200 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('B=$B', round(d['roofline']['avg_launch_us'],2), 'us', d['launch'])"; RAAS_CLUSTER=0 timeout 300 python bench.py --config 2 --batch $B --steps 200 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('B=$B nocl', round(d['roofline']['avg_launch_us'],2), 'us', d['launch'])"; done
+cp paper_2502_11147_b200/libraas.so build_exp/libraas_cur.so
+bash scripts/ab.sh "--config 2 --steps 200;--steps 60;--config 4 --steps 40;--config 5 --L 256 --layers 8 --steps 100" 2 build_exp/libraas_cur.so build_exp/libraas_pre16.so 2>&1 | grep "|"
