@@ -301,10 +301,10 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
     // after_copies: staged cudaMemcpyAsync copies precede this launch (full serialisation).
     // The zero-copy ingest kernel triggers us at its start, so it does not count: the kernel
     // two back has completed, the one right before (this handle's or not) may still run.
-    // not with the Quest-on-prefill hybrid: its selection kernel (this handle's) runs right
-    // before the decode kernel and writes the attended-page list the producer reads; not when
-    // the caller opted out (raas.h "Early start")
-    p.early = (other || after_copies) && h->cfg.quest_prefill_pages == 0 && !h->cfg.disable_early_start;
+    // the Quest-on-prefill hybrid's selection kernel (this handle's) runs right before the decode
+    // kernel and writes the attended-page list: the producer issues only the pages that do not
+    // depend on it before the wait; not when the caller opted out (raas.h "Early start")
+    p.early = (other || after_copies) && !h->cfg.disable_early_start;
   }
   p.cl = h->cl;
   p.n_kv = h->cfg.n_kv_heads;

@@ -911,7 +911,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
   // completed before the previous one could trigger us, so the producer reads its first tile's
   // metadata and issues that tile's first page copies BEFORE griddepcontrol.wait (below); only
   // the step's inputs (q, k_new, v_new) and every store wait for the previous kernel.
-  const bool early = p.early != 0;  // never with the Quest-on-prefill hybrid (host)
+  const bool early = p.early != 0;  // hybrid: only its selection-independent pages (producer)
   if (!(early && warp == 0)) {
     pdl_wait();  // everything above overlapped the previous kernel; state reads start here
     pdl_launch_dependents();
@@ -973,7 +973,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
     // a tile covers the "attended page list" positions v in [split*SP, split*SP + SP): the
     // resident pages in index order, or, in the Quest-on-prefill hybrid (NEXT-4), the K
     // selected full prompt pages (from raas_qselect) followed by every page from nfull on
-    int nphys = 0, nnatt = 0;
+    int nphys = 0, nnatt = 0, nndep = 0;  // nndep: leading positions independent of the selection
     auto fetch = [&](int tl) {
       if (tl < n_tiles) {
         const int u = tl / p.nsplit, q0 = (tl - u * p.nsplit) * SP;
@@ -988,8 +988,12 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
           nphys = v;
           ncnt = (lane < SP && v < nnatt) ? min(PAGE, nplan.z - PAGE * v) : 0;
         } else {
+          // hybrid: the pages from nfull on first (they do not depend on this step's selection,
+          // so an early start can issue them before griddepcontrol.wait), then the K selected
+          // prompt pages, read only after the selection kernel (the previous grid) completed
           nnatt = hyb ? quest_k + nplan.z - nf : nplan.z;
-          nphys = !hyb ? v : (v < quest_k ? p.vmap[(size_t)u * C + v] : nf + (v - quest_k));
+          nndep = hyb ? nplan.z - nf : nnatt;
+          nphys = !hyb ? v : v < nndep ? nf + v : v < nnatt ? __ldcg(p.vmap + (size_t)u * C + (v - nndep)) : 0;
           ncnt = (lane < SP && v < nnatt) ? __ldcg(p.cnt + (size_t)u * C + nphys) : 0;
         }
       }
@@ -1046,11 +1050,14 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
           // the whole first tile when the ring holds it (16-page tiles: small budgets, B = 1;
           // -1 % there), else one batch (32-page tiles: a second batch early cost config 4 +0.6 %)
           pre = RAAS_PRE > 0 ? min(n, RAAS_PRE < S ? RAAS_PRE : S) : (n <= S ? n : min(n, BATCH));
-          issue_batch(0, pre, 0, unit, n, 0, ncnt, nphys, nplan.x, nplan.y & 0xffff);
+          // hybrid: only the positions before nndep are final before the wait
+          if (quest_k > 0) pre = max(0, min(pre, nndep - p0));
+          if (pre > 0) issue_batch(0, pre, 0, unit, n, 0, ncnt, nphys, nplan.x, nplan.y & 0xffff);
         }
       }
       pdl_wait();
       pdl_launch_dependents();
+      if (quest_k > 0 && tile >= 0) fetch(tile);  // the selected pages of the first tile, now final
     }
     while (tile >= 0) {
       const int unit = tile / p.nsplit, split = tile - unit * p.nsplit;
