@@ -75,7 +75,7 @@ def compare_state(g, o, alpha, pstar, res, layer, resync=True, top_r=None, histo
         layer.raas_set_state(o["t"], o["ts"], o["start"], o["count"], o["pinned"])
 
 
-def compare_sampled(layer, orc, units, alpha, pstar, res):
+def compare_sampled(layer, orc, units, alpha, pstar, res, top_r=None):
     """Full-size lockstep on sampled units: the oracle holds only `units` of the GPU handle.
     Their state must be bit-exact (a differing timestamp only inside the band, counted, then
     the GPU rows are resynced to the oracle's)."""
@@ -89,6 +89,10 @@ def compare_sampled(layer, orc, units, alpha, pstar, res):
         assert np.array_equal(g[k], os_[k]), f"state field {k} differs outside the stamp band"
     for u, p in np.argwhere(g["ts"] != os_["ts"]):
         ps = pstar[u, p]
+        if top_r is not None:
+            assert _topr_band(pstar[u], p, top_r), f"top-r decision differs at sampled unit {units[u]} page {p}"
+            res.band_events += 1
+            continue
         assert ps >= 0 and abs(ps - alpha) < BAND, (
             f"ts differs at sampled unit {units[u]} page {p}: gpu {g['ts'][u, p]} oracle "
             f"{os_['ts'][u, p]}, p*={ps!r} outside the |p*-alpha|<{BAND} band")

@@ -363,6 +363,57 @@ def test_full_size_sampled_units_lockstep(oracle_mod, cfg, B, Hq, Hkv, L, P, sp,
     assert layer.raas_get_status() == 0
 
 
+@pytest.mark.parametrize("kw,lam", [
+    ({"score_mode": 1}, 9.0),                               # NEXT-1 Quest bound scores
+    ({"stamp_rule": 1, "top_r": 0.5}, 7.0),                  # NEXT-3 top-r (r = 0.5, :135)
+    ({"table_scope": 1}, 11.0),                              # NEXT-2 one table per request (38 %)
+    ({"table_scope": 1, "stamp_rule": 1, "top_r": 0.5}, 7.0),
+])
+def test_full_size_variants_sampled_lockstep(oracle_mod, kw, lam):
+    """The method variants in bench.py's launch configuration at config 3 (B = 64, L = 2048,
+    Llama heads): full batch on the GPU from a full-cache waterfall state, first and last request
+    on the oracle in lockstep for 40 steps (per-request tables: every kv-head of a request starts
+    from the same replica)."""
+    B, Hq, Hkv, d, L, P, T = 64, 32, 8, 128, 2048, 256, 40
+    state, kst, vst, steps = waterfall_resume(500 + int(lam), B, Hq, Hkv, d, L, P, T, cur_count=9, lam=lam)
+    if kw.get("table_scope"):
+        for k in ("t", "ts", "start", "count", "pinned"):
+            v = state[k].reshape(B, Hkv, *state[k].shape[1:])
+            state[k] = np.ascontiguousarray(np.repeat(v[:, :1], Hkv, axis=1).reshape(state[k].shape))
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B, **kw)
+    layer.raas_set_state(state["t"], state["ts"], state["start"], state["count"], state["pinned"],
+                         kst, vst)
+    sample = [0, B - 1]
+    units = [b * Hkv + h for b in sample for h in range(Hkv)]
+    orc = oracle_mod.Oracle(L=L, alpha=1e-4, page=PAGE, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
+                            batch=len(sample), **kw)
+    orc.set_state(*(state[k][units] for k in ("t", "ts", "start", "count", "pinned")),
+                  kst[units], vst[units])
+    del kst, vst
+    res = LockstepResult()
+    out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
+    top_r = kw.get("top_r") if kw.get("stamp_rule") == 1 else None
+    for i in range(T):
+        layer.raas_decode_step(to_dev(steps.q[i]), to_dev(steps.k[i]), to_dev(steps.v[i]), out)
+        o_out = orc.decode_step(steps.q[i][sample], steps.k[i][sample], steps.v[i][sample])
+        g_out = bf16_to_f32(from_dev(out)).astype(np.float64)[sample]
+        res.max_err = max(res.max_err, float(np.abs(g_out - o_out).max()))
+        tr = orc.get_trace()
+        res.evictions += int((tr["evicted"] >= 0).sum())
+        res.stamp_decisions += int((tr["pstar"] >= 0).sum())
+        res.stamps += int((tr["pstar"] > 1e-4).sum())
+        compare_sampled(layer, orc, units, 1e-4, tr["pstar"], res, top_r=top_r)
+    assert res.band_events == 0 and res.max_err <= OUT_TOL
+    assert res.evictions >= len(units) * 2
+    c = layer.raas_get_counters()
+    # the Quest bound stamps (nearly) every page of this stream at alpha = 1e-4: its decisions
+    # are far from the threshold, so it is the bound's arithmetic, not the band, that is checked
+    assert 0 < c["stamps"] <= c["decisions"]
+    if not kw.get("score_mode"):
+        assert c["stamps"] < c["decisions"]
+    assert layer.raas_get_status() == 0
+
+
 def test_max_budget_lockstep(oracle_mod):
     """The largest budget one handle supports at the default split size: L = 80 splits x 32
     pages x 16 = 40960 tokens (MAX_SPLITS partials per unit), from a full-cache waterfall state
