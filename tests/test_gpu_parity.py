@@ -203,16 +203,18 @@ def test_head_sharding_bitwise():
     assert s_full["count"].sum() > 0
 
 
-@pytest.mark.parametrize("mode", ["pinned_reused", "pinned_queued", "pageable"])
-def test_host_entry_point_matches_device_entry_point(mode):
+@pytest.mark.parametrize("mode,sp", [("pinned_reused", 0), ("pinned_queued", 0), ("pageable", 0),
+                                     ("pinned_queued", 1)])   # 1-page splits: cluster schedule
+def test_host_entry_point_matches_device_entry_point(mode, sp):
     """raas_decode_step_host: pinned buffers take the zero-copy path (ingest kernel + out
     stored straight to host memory), pageable ones the staged copies; both are bitwise the
     device entry point.  'reused' rewrites one pinned buffer every step (no stale reads);
     'queued' enqueues every step before one synchronisation (stream order kept)."""
     B, Hq, Hkv, d, P, T, L = 2, 8, 2, 128, 40, 40, 64
     st = waterfall_stream(4, B, Hq, Hkv, d, P, T)
-    dev, s_dev = _run_gpu(st, L, Hq, Hkv)
-    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
+    dev, s_dev = _run_gpu(st, L, Hq, Hkv, split_pages=sp)
+    layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B, split_pages=sp)
+    assert layer.raas_launch_info()["cluster"] == (4 if sp == 1 else 1)
     layer.raas_prefill(to_dev(st.k_pre), to_dev(st.v_pre), P)
 
     def host(x, pin):
@@ -819,8 +821,9 @@ def test_token_level_alpha_extremes(oracle_mod, alpha):
 @pytest.mark.parametrize("kw", [
     {}, {"score_mode": 1}, {"stamp_rule": 1, "top_r": 0.5}, {"table_scope": 1},
     {"page": 1}, {"page": 1, "stamp_rule": 1, "top_r": 0.5}, {"quest_prefill_pages": 1},
-    {"disable_early_start": 1},
-], ids=["default", "quest", "top_r", "table", "token_tokd", "token_top_r", "hybrid", "no_early"])
+    {"disable_early_start": 1}, {"split_pages": 2},
+], ids=["default", "quest", "top_r", "table", "token_tokd", "token_top_r", "hybrid", "no_early",
+        "cluster"])
 def test_interleaved_handles_early_start_matches_single_handle_runs(kw):
     """Layers interleaved on one stream (the model's order) take the early-start path: each
     launch reads its handle's state before griddepcontrol.wait, since the previous kernel is
