@@ -36,6 +36,10 @@ def main():
     print(f"overlap of launch k's end with launch k+1's start: median {statistics.median(ov):.1f} us "
           f"(positive = k+1 started before k ended)")
     print(f"period (first start -> last end) / launches: {period:.1f} us")
+    if other:
+        od = [e["dur"] for e in other]
+        names = sorted({e["name"].split("(")[0][:60] for e in other})
+        print(f"other kernels: {len(other)}, median {statistics.median(od):.1f} us ({', '.join(names)})")
     print("first launches (us from the first start): start, end, duration")
     for e in ks[: min(len(ks), 6)]:
         print(f"  {e['ts'] - t0:9.1f} {e['ts'] + e['dur'] - t0:9.1f} {e['dur']:7.1f}")
