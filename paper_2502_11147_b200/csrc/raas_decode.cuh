@@ -573,6 +573,7 @@ __device__ __forceinline__ void combine_unit_cl(const DecodeParams& p, int unit,
   const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
   const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
   mbar_wait_cluster(clbar, 0);  // every split's partial and page maxima are here
+  RAAS_COMB_MARK(0);
   // ---- a5 (1): running merge of the split statistics -> factors, LSE, 1 / l ----
   if (lane < g) {
     float m = -INFINITY, l = 0.f;
@@ -590,24 +591,36 @@ __device__ __forceinline__ void combine_unit_cl(const DecodeParams& p, int unit,
   }
   __syncwarp();
   // ---- a5 (2): out[h][d] = acc[h][d] / l_h, acc folded in split order ----
-  constexpr int CPH = D / 4;
+  constexpr int CPH = D / 4;  // float4 chunks per head; a lane's 4 chunks per round share a head
   const int nch = g * CPH;
-  for (int c = lane; c < nch; c += 32) {
-    const int h = c / CPH, d4 = c - h * CPH;
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c0 = 4 * lane; c0 < nch; c0 += 128) {  // 4 consecutive chunks per lane per round
+    const int h = c0 / CPH, d40 = c0 - h * CPH;
+    float4 o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < nse; ++s) {
-      const float4 v = lds_f32x4(recv + s * RSLOT + PUB_ACC_OFF + (h * D + 4 * d4) * 4);
       const float fa = lds_f32(scr_w + 8 * (s * g + h)), fb = lds_f32(scr_w + 8 * (s * g + h) + 4);
-      o.x = fmaf(o.x, fa, __fmul_rn(v.x, fb));
-      o.y = fmaf(o.y, fa, __fmul_rn(v.y, fb));
-      o.z = fmaf(o.z, fa, __fmul_rn(v.z, fb));
-      o.w = fmaf(o.w, fa, __fmul_rn(v.w, fb));
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = lds_f32x4(recv + s * RSLOT + PUB_ACC_OFF + (h * D + 4 * (d40 + k)) * 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        o[k].x = fmaf(o[k].x, fa, __fmul_rn(v[k].x, fb));
+        o[k].y = fmaf(o[k].y, fa, __fmul_rn(v[k].y, fb));
+        o[k].z = fmaf(o[k].z, fa, __fmul_rn(v[k].z, fb));
+        o[k].w = fmaf(o[k].w, fa, __fmul_rn(v[k].w, fb));
+      }
     }
     const float inv = lds_f32(scr_inv + 4 * h);
-    *reinterpret_cast<uint2*>(p.out + (size_t)(unit * g + h) * D + 4 * d4) =
-        make_uint2(pack_bf16x2(o.x * inv, o.y * inv), pack_bf16x2(o.z * inv, o.w * inv));
+#pragma unroll
+    for (int k = 0; k < 4; k += 2)
+      *reinterpret_cast<uint4*>(p.out + (size_t)(unit * g + h) * D + 4 * (d40 + k)) =
+          make_uint4(pack_bf16x2(o[k].x * inv, o[k].y * inv), pack_bf16x2(o[k].z * inv, o[k].w * inv),
+                     pack_bf16x2(o[k + 1].x * inv, o[k + 1].y * inv),
+                     pack_bf16x2(o[k + 1].z * inv, o[k + 1].w * inv));
   }
   // ---- a6: stamp; a2 metadata of the write slot; a7 candidates ----
+  RAAS_COMB_MARK(1);
   float lse[MAX_GROUP];
 #pragma unroll
   for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
@@ -646,9 +659,11 @@ __device__ __forceinline__ void combine_unit_cl(const DecodeParams& p, int unit,
       }
     }
   }
+  RAAS_COMB_MARK(2);
   const int victim = warp_argmin_page(best);
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
+  RAAS_COMB_MARK(3);
   if (lane == 0) {
     p.plan[unit] = next_plan(slot, off + 1, used_eff, C, t, victim, p.status, PAGE);
     atomicAdd(p.stats + 0, (unsigned long long)n_stamp);
@@ -1336,9 +1351,17 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RA
         entry = __shfl_sync(0xffffffffu, entry, 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(cqempty(i % CQ));
-        if (entry >= 0)
-          combine_unit_cl<D>(p, entry & ((1 << CQ_UNIT_BITS) - 1), (entry >> CQ_UNIT_BITS) & CQ_NSE_MASK,
-                             scr, lane, recv, recv + p.nsplit * Lay::RECV_SLOT, clfull, cm);
+        if (entry >= 0) {
+          const int unit_e = entry & ((1 << CQ_UNIT_BITS) - 1);
+#ifdef RAAS_DBG_TIMING
+          if (lane == 0 && unit_e < 4096) { g_raas_dbg_unit[unit_e][0] = blockIdx.x; g_raas_dbg_unit[unit_e][2] = dbg_gtimer(); }
+#endif
+          combine_unit_cl<D>(p, unit_e, (entry >> CQ_UNIT_BITS) & CQ_NSE_MASK, scr, lane, recv,
+                             recv + p.nsplit * Lay::RECV_SLOT, clfull, cm);
+#ifdef RAAS_DBG_TIMING
+          if (lane == 0 && unit_e < 4096) g_raas_dbg_unit[unit_e][3] = dbg_gtimer();
+#endif
+        }
       }
     } else {
       combine_loop(scr);
