@@ -57,6 +57,14 @@ template <int D, bool TOKD, bool GEN>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD, GEN>; }
 template <int D>
 constexpr auto decode_kernel_cl() { return raas::raas_decode_kernel<D, NC, S, false, false, true>; }
+// one-split units of <= 16 pages (L <= 256 at the default split size; the default method): a half-size CTA
+// (4 consumers, 8 stages, 114 KB) so that two fit on an SM and the next layer's CTA streams
+// beside the current one's tail (profiles/r02_study.md §6, §10)
+constexpr int NC2 = 4, S2 = 8;
+template <int D>
+constexpr auto decode_kernel_half() { return raas::raas_decode_kernel<D, NC2, S2, false, false>; }
+template <int D>
+using LayHalf = raas::DecodeLayout<D, NC2, S2, false, false>;
 
 struct Layout {
   size_t kvstore, ts, start, cnt, npin, nfull, plen, plan, repkey, vmap, counter, req_x, req_ctr,
@@ -228,6 +236,7 @@ struct raas_handle {
   int num_sms;
   int grid;
   int cl;  // cluster schedule (DecodeParams::cl): grid = units * nsplit, clusters of nsplit
+  int half;  // half-size CTAs, two per SM (one-split units of the default method)
   int smem;
   uint8_t* arena;
   int prefilled;
@@ -333,7 +342,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(h->grid);
-  lc.blockDim = dim3(Lay<D>::THREADS);  // the same for both instantiations
+  lc.blockDim = dim3(h->half ? LayHalf<D>::THREADS : Lay<D>::THREADS);
   lc.dynamicSmemBytes = h->smem;
   lc.stream = st;
   cudaLaunchAttribute attr[2];
@@ -348,6 +357,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   if (h->d.tokd)     RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true, false>(), p));
   else if (h->d.gen) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, true>(), p));
   else if (h->cl)    RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_cl<D>(), p));
+  else if (h->half)  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_half<D>(), p));
   else               RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, false>(), p));
   return RAAS_OK;
 }
@@ -438,6 +448,22 @@ int setup_kernel(raas_handle* h) {
   if (want_cl) {
     int rc = setup_kernel_t<D, false, false>(h, true);
     if (rc || h->cl) return rc;  // else clusters of this size do not fit: default schedule
+  }
+  // units of one tile of <= 16 pages: L = 256 17.8 -> 17.0 us; 32-page tiles (L = 512) lose
+  // (26.4 -> 27.2 us: 8 pages per consumer on half the consumers)
+  bool want_half = h->d.nsplit == 1 && h->d.split_pages <= 16;
+  if (const char* e = std::getenv("RAAS_HALF")) want_half = want_half && std::atoi(e) != 0;  // A/B, tests
+  if (want_half) {
+    auto k = decode_kernel_half<D>();
+    h->smem = LayHalf<D>::SMEM;
+    RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
+    int per_sm = 0;
+    RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LayHalf<D>::THREADS, h->smem));
+    if (per_sm >= 2) {
+      h->half = 1;
+      h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
+      return RAAS_OK;
+    }
   }
   return setup_kernel_t<D, false, false>(h, false);
 }
@@ -868,7 +894,8 @@ RAAS_API int raas_debug_tokd(int32_t* out16) {
 int raas_launch_info(const raas_handle* h, int32_t info[6]) {
   if (!h || !info) return fail(RAAS_E_INVALID, "null argument");
   info[0] = h->grid;
-  info[1] = h->cfg.head_dim == 128 ? Lay<128>::THREADS : Lay<64>::THREADS;
+  info[1] = h->half ? (h->cfg.head_dim == 128 ? LayHalf<128>::THREADS : LayHalf<64>::THREADS)
+                    : (h->cfg.head_dim == 128 ? Lay<128>::THREADS : Lay<64>::THREADS);
   info[2] = h->smem;
   info[3] = h->d.split_pages;
   info[4] = h->d.nsplit;

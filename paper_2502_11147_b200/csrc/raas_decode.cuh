@@ -840,7 +840,7 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 __device__ int g_tokd_dbg[16];
 #endif
 template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false>
-__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, RAAS_MINB)
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (NC <= 4 ? 2 : RAAS_MINB))
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
   // CL: the cluster-schedule instantiation of the default method (small batches); the other
   // instantiations carry none of its code (registers: see DESIGN.md §6)
