@@ -433,9 +433,9 @@ int setup_kernel_t(raas_handle* h, bool want_cl) {
 template <int D>
 int setup_kernel(raas_handle* h) {
   if (h->d.tokd) return setup_kernel_t<D, true, false>(h, false);
-  if (std::getenv("RAAS_FORCE_GEN")) h->d.gen = 1;  // A/B experiments: the generic instantiation
-  // cluster schedule (generic instantiation) when the (unit, split) tiles fit the SMs one per
-  // CTA and every unit is split; RAAS_CLUSTER=0 disables it (A/B experiments, tests)
+  // cluster schedule (its own instantiation of the default method) when the (unit, split) tiles
+  // fit the SMs one per CTA and every unit is split; RAAS_CLUSTER=0 disables it (A/B
+  // experiments and the schedule-equivalence tests; numerics never depend on it)
   const long long tiles = (long long)h->d.units * h->d.nsplit;
   // the leader's receive area holds nsplit partials and the unit's page maxima [C][g] fp32,
   // and its combine's preloaded metadata covers C <= 32 * CLM pages
