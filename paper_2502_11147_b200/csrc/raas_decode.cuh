@@ -1570,6 +1570,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (N
         __syncwarp();
         mbar_arrive(empty(s));  // stage free for the producer
       };
+#ifdef RAAS_DBG_HOLD  // sensitivity probe: the stage held longer before its release
+      {
+        const long long t0 = clock64();
+        while (clock64() - t0 < RAAS_DBG_HOLD) {
+        }
+      }
+#endif
       if (score_mode == 0) release_stage();
       if constexpr (TOKD) {
         // deferred a6 (step t-1's stamps, PAPER.md :98-100 at token level) and a7 candidates:
@@ -1742,6 +1749,13 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (N
       const uint32_t b1 = movmatrix_t(pack_bf16x2(p2, p3));
 #pragma unroll
       for (int mt = 0; mt < KS; ++mt) mma_bf16_16816(acc[mt], va[mt], b0, b1);
+#ifdef RAAS_DBG_DELAY  // sensitivity probe: extra consumer time per page (after the release)
+      {
+        const long long t0 = clock64();
+        while (clock64() - t0 < RAAS_DBG_DELAY) {
+        }
+      }
+#endif
 
       if (flags & FLAG_LAST) {  // deposit this warp's softmax state for the tile merge
 #pragma unroll
