@@ -208,13 +208,11 @@ RAAS_API int raas_get_status(raas_handle* h, void* stream);
  * (unpinned resident pages examined), [2] evictions, [3] unit-steps.  Synchronises. */
 RAAS_API int raas_get_counters(raas_handle* h, uint64_t counters[4], void* stream);
 
-/* Launch shape of the decode kernel (for roofline accounting): [0] grid CTAs, [1] threads per
- * CTA, [2] dynamic shared memory bytes, [3] split pages, [4] splits per unit, [5] thread-block
- * cluster size (1: the default persistent schedule; nsplit: the cluster schedule for small
- * batches, where each unit's split CTAs exchange their partials through distributed shared
- * memory), [6] 1 when the tail-pool schedule runs (fewer units than CTAs: each unit's last
- * split streams on a spare CTA), [7] reserved (0).  The schedule never changes results. */
-RAAS_API int raas_launch_info(const raas_handle* h, int32_t info[8]);
+/* Launch shape of the decode kernel (for roofline accounting): grid CTAs, threads per CTA,
+ * dynamic shared memory bytes, split pages, splits per unit, thread-block cluster size (1: the
+ * default persistent schedule; nsplit: the cluster schedule for small batches, where each
+ * unit's split CTAs exchange their partials through distributed shared memory). */
+RAAS_API int raas_launch_info(const raas_handle* h, int32_t info[6]);
 
 /* Thread-local message describing the last error (never NULL). */
 RAAS_API const char* raas_last_error(void);

@@ -237,7 +237,6 @@ struct raas_handle {
   int grid;
   int cl;  // cluster schedule (DecodeParams::cl): grid = units * nsplit, clusters of nsplit
   int half;  // half-size CTAs, two per SM (one-split units of the default method)
-  int tp;    // tail-pool schedule (DecodeParams::tp)
   int smem;
   uint8_t* arena;
   int prefilled;
@@ -317,7 +316,6 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
     p.early = (other || after_copies) && !h->cfg.disable_early_start;
   }
   p.cl = h->cl;
-  p.tp = h->tp;
   p.n_kv = h->cfg.n_kv_heads;
   p.req_x = h->cfg.table_scope ? reinterpret_cast<uint32_t*>(a + h->lay.req_x) : nullptr;
   p.req_ctr = h->cfg.table_scope ? reinterpret_cast<int32_t*>(a + h->lay.req_ctr) : nullptr;
@@ -369,9 +367,8 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
 // the cross-CTA combine that ends the kernel (~8 us, expressed in tiles of SP pages streamed at
 // ~48 GB/s per SM: 8 KiB per page).  The result never changes numerics (the split arithmetic is
 // schedule-free), only the speed.
-int choose_grid(int units, int nsplit, int sp, int cap, int* tp = nullptr) {
+int choose_grid(int units, int nsplit, int sp, int cap) {
   const long long tiles = (long long)units * nsplit;
-  if (tp) *tp = 0;
   if (tiles <= 0) return 1;
   const double tile_us = sp * 8192.0 / 48e3;  // us per tile
   const double tail_tiles = 8.0 / tile_us;
@@ -389,22 +386,6 @@ int choose_grid(int units, int nsplit, int sp, int cap, int* tp = nullptr) {
       best = G;
     }
   }
-  // Tail-pool schedule (units < G): CTA b < units streams unit b's first nsplit - 1 splits,
-  // the G - units spare CTAs share the units' last splits; the owner's prefix and the last
-  // split meet in L2 (~two dependent round trips at the owner's end, ~1 us).  Config 4 (128
-  // units of 8 splits): 8 tiles per CTA on 128 SMs -> 7 on all 148.
-  if (tp && nsplit >= 2) {
-    const double meet_tiles = 1.0 / tile_us;
-    for (int G = units + 1; G <= cap; ++G) {
-      const int s = G - units;
-      const double cost = (double)std::max(nsplit - 1, (units + s - 1) / s) + meet_tiles;
-      if (cost < best_cost - 1e-9 || (*tp && cost < best_cost + 1e-9 && G > best)) {
-        best_cost = cost;
-        best = G;
-        *tp = 1;
-      }
-    }
-  }
   return best;
 }
 
@@ -416,21 +397,10 @@ int setup_kernel_t(raas_handle* h, bool want_cl) {
   int per_sm = 0;
   RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD, GEN>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
-  // tail pool: not for the deferred token-level kernel (its split partials carry victim keys)
-  bool want_tp = !TOKD;
-  int pool_env = -1;  // RAAS_POOL=0 off, =2 forced wherever units < grid cap (A/B, tests)
-  if (const char* e = std::getenv("RAAS_POOL")) pool_env = std::atoi(e);
-  if (pool_env == 0) want_tp = false;
-  const int cap = h->num_sms * per_sm;
-  h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, cap, want_tp ? &h->tp : nullptr);
-  if (want_tp && pool_env == 2 && h->d.nsplit >= 2 && h->d.units < cap) {
-    h->tp = 1;  // spares = units / 2 (each grabs about two last splits)
-    h->grid = std::min(cap, h->d.units + std::max(1, h->d.units / 2));
-  }
+  h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
   if (const char* e = std::getenv("RAAS_GRID")) {  // tuning experiments only (scripts/)
     const int G = std::atoi(e);
-    if (G > 0) h->grid = std::min(G, cap);
-    if (G > 0) h->tp = 0;
+    if (G > 0) h->grid = std::min(G, h->num_sms * per_sm);
   }
   // Cluster schedule when the (unit, split) tiles fit the SMs one per CTA and every unit is
   // split (small batches, e.g. config 2 at B = 1): each unit's nsplit CTAs form a cluster and
@@ -453,7 +423,6 @@ int setup_kernel_t(raas_handle* h, bool want_cl) {
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, k, &lc) == cudaSuccess && nclusters > 0) {
       h->cl = 1;
-      h->tp = 0;
       h->grid = (int)tiles;
     } else {
       cudaGetLastError();  // clusters of this size do not fit: keep the default schedule
@@ -492,7 +461,6 @@ int setup_kernel(raas_handle* h) {
     RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LayHalf<D>::THREADS, h->smem));
     if (per_sm >= 2) {
       h->half = 1;
-      h->tp = 0;
       h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
       return RAAS_OK;
     }
@@ -923,7 +891,7 @@ RAAS_API int raas_debug_tokd(int32_t* out16) {
   return cudaMemcpyFromSymbol(out16, raas::g_tokd_dbg, 64) == cudaSuccess ? 0 : 1;
 }
 #endif
-int raas_launch_info(const raas_handle* h, int32_t info[8]) {
+int raas_launch_info(const raas_handle* h, int32_t info[6]) {
   if (!h || !info) return fail(RAAS_E_INVALID, "null argument");
   info[0] = h->grid;
   info[1] = h->half ? (h->cfg.head_dim == 128 ? LayHalf<128>::THREADS : LayHalf<64>::THREADS)
@@ -932,8 +900,6 @@ int raas_launch_info(const raas_handle* h, int32_t info[8]) {
   info[3] = h->d.split_pages;
   info[4] = h->d.nsplit;
   info[5] = h->cl ? h->d.nsplit : 1;
-  info[6] = h->tp;
-  info[7] = 0;
   return RAAS_OK;
 }
 
@@ -943,6 +909,8 @@ RAAS_API int raas_debug_units(uint64_t* out, int n) {
   RAAS_CUDA(cudaMemcpyFromSymbol(out, raas::g_raas_dbg_unit, sizeof(uint64_t) * (n < 4096 * 4 ? n : 4096 * 4)));
   if (n >= 4096 * 8)
     RAAS_CUDA(cudaMemcpyFromSymbol(out + 4096 * 4, raas::g_raas_dbg_comb, sizeof(uint64_t) * 4096 * 4));
+  if (n >= 4096 * 16)
+    RAAS_CUDA(cudaMemcpyFromSymbol(out + 4096 * 8, raas::g_raas_dbg_cyc, sizeof(uint64_t) * 4096 * 8));
   return RAAS_OK;
 }
 RAAS_API int raas_debug_timeline(uint64_t* out, int n) {  // [8][256][4], then cleared

@@ -66,7 +66,11 @@ __device__ __forceinline__ void dbg_add(int, long long) {}
 #ifdef RAAS_DBG_TIMING
 #define RAAS_COMB_MARK(i) \
   do { if (lane == 0 && unit < 4096) g_raas_dbg_comb[unit][i] = dbg_gtimer(); } while (0)
+__device__ long long g_raas_dbg_cyc[4096][8];  // combine: SM cycles at fine marks
+#define RAAS_CYC(i) \
+  do { if (lane == 0 && unit < 4096) g_raas_dbg_cyc[unit][i] = clock64(); } while (0)
 #else
+#define RAAS_CYC(i) do {} while (0)
 #define RAAS_COMB_MARK(i) do {} while (0)
 #endif
 #define RAAS_TIMED(slot, stmt)          \
@@ -107,18 +111,14 @@ __device__ __forceinline__ void merge_factors(float m, float ms, float& mn, floa
 // counter for the next launch.
 // Cluster schedule (cl): CTA b streams tile b only, i.e. split b % nsplit of unit b / nsplit
 // (the cluster of the unit's nsplit consecutive CTAs).
-// Tail-pool schedule (tp; units < G, e.g. config 4: 128 units on 148 SMs): CTA b < units owns
-// unit b's splits 0 .. nsplit-2; the last split of every unit forms a pool that only the
-// G - units spare CTAs grab (dynamically), so every SM streams and no CTA streams a whole
-// unit.  The owner's prefix and the pool split's partial meet wait-free (merge warp).
 struct TileSched {
   int b, G, fu, nsplit, n_owned, n_shared_tiles, shared_base, i_owned;
-  bool cl, tp;
-  __device__ TileSched(int units, int nsplit_, int G_, int b_, bool cl_, bool tp_)
-      : b(b_), G(G_), nsplit(nsplit_), cl(cl_), tp(tp_) {
-    fu = (cl || tp) ? 0 : units / G;
-    n_owned = tp ? (b < units ? nsplit - 1 : 0) : fu * nsplit;
-    n_shared_tiles = cl ? 0 : tp ? (b < units ? 0 : units) : (units - fu * G) * nsplit;
+  bool cl;
+  __device__ TileSched(int units, int nsplit_, int G_, int b_, bool cl_)
+      : b(b_), G(G_), nsplit(nsplit_), cl(cl_) {
+    fu = cl ? 0 : units / G;
+    n_owned = fu * nsplit;
+    n_shared_tiles = cl ? 0 : (units - fu * G) * nsplit;
     shared_base = fu * G * nsplit;
     i_owned = 0;
   }
@@ -130,7 +130,7 @@ struct TileSched {
     }
     if (i_owned < n_owned) {
       owned = true;
-      return tp ? b * nsplit + i_owned++ : b * n_owned + i_owned++;
+      return b * n_owned + i_owned++;
     }
     // a grabbed tile of a one-split unit is the whole unit: it takes the owned path (out and
     // LSE from the merge warp, no partial through L2), whichever CTA grabs it
@@ -139,7 +139,6 @@ struct TileSched {
     int x = 0;
     if (lane == 0) x = atomicAdd(grab, 1);
     x = __shfl_sync(0xffffffffu, x, 0);
-    if (tp) return x < n_shared_tiles ? x * nsplit + nsplit - 1 : -1;  // a unit's last split
     return x < n_shared_tiles ? shared_base + x : -1;
   }
 };
@@ -282,6 +281,8 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
   const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
   const float2* ml_g = p.part_ml + (size_t)unit * p.nsplit * g;
+  RAAS_CYC(0);
+  RAAS_CYC(1);
   const int4 pl = __ldcg(p.plan + unit);
   const int npin = __ldg(p.npin + unit);
   float2 mla[2];
@@ -322,6 +323,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     }
   };
   load_meta(0, C);
+  RAAS_CYC(2);
   // first block of split partials: 4 float4 chunks per lane x 2 splits
   constexpr int CPH = D / 4;                   // chunks per head
   constexpr int CB = 4, SG = 2;
@@ -342,6 +344,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     }
   };
   load_acc(0, 0);
+  RAAS_CYC(3);
   // ---- a5 (1): running merge of the split statistics -> per-split factors, LSE, 1 / l ----
   if (!outdone) {
 #pragma unroll
@@ -376,6 +379,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   }
   __syncwarp();
   RAAS_COMB_MARK(0);
+  RAAS_CYC(4);
   float lse[MAX_GROUP];
 #pragma unroll
   for (int h = 0; h < MAX_GROUP; ++h) lse[h] = h < g ? lds_f32(scr_lse + 4 * h) : 0.f;
@@ -535,6 +539,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     }
   }
   RAAS_COMB_MARK(2);
+  RAAS_CYC(5);
   const int victim = warp_argmin_page(best);
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
@@ -550,6 +555,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
       atomicAdd(p.stats + 3, 1ull);
     }
   }
+  RAAS_CYC(6);
 }
 
 
@@ -912,9 +918,9 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (N
     // Warm L2 with this CTA's first owned tile while the previous kernel drains (its tail
     // leaves HBM idle).  Only a hint: nothing is read from these lines before griddepcontrol.wait
     // below, and L2 is the point of coherence, so a row the previous kernel rewrites is seen.
-    const int fu = p.tp ? ((int)blockIdx.x < p.units ? 1 : 0) : p.units / (int)gridDim.x;
+    const int fu = p.units / (int)gridDim.x;
     if (fu > 0) {
-      const int unit0 = p.tp ? (int)blockIdx.x : blockIdx.x * fu;
+      const int unit0 = blockIdx.x * fu;
       // about an eighth of the CTA's owned tiles, 1..RAAS_PREFETCH_TILES (config 3, 12 owned
       // tiles: 2; config 4 and the small budgets, 4-8: 1; L = 4096 / 8192, 24 / 48: 3 / 4;
       // measured per config, see profiles/r01_schedule_study.md)
@@ -1055,7 +1061,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (N
       }
       __syncwarp();
     };
-    TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x, cl, !TOKD && !cl && p.tp != 0);
+    TileSched sched(p.units, p.nsplit, gridDim.x, blockIdx.x, cl);
     bool owned = false, owned_next = false;
     int tile = sched.next(p.sched, lane, owned);
     if (tile >= 0) fetch(tile);
@@ -1236,83 +1242,30 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (N
       }
       __syncwarp();
       mbar_arrive(tfree(par));  // deposits / q / info of tile k consumed (each lane's reads)
-      // tail-pool schedule (p.tp): the unit's last split ran on a spare CTA ("pool" tile here)
-      const bool pool = !TOKD && p.tp && !owned;
-      if (!TOKD && (owned || pool)) {
+      if (!TOKD && owned) {
         // an owned unit's splits arrive here in order on this CTA: fold the tile into the
         // running merge; after the last split write out and hand the LSE to the combine
-        auto fold = [&]() {
-          float mn0, fa0, fb0, mn1, fa1, fb1;
-          merge_factors(rm0, M0, mn0, fa0, fb0);
-          merge_factors(rm1, M1, mn1, fa1, fb1);
-          rl0 = fmaf(rl0, fa0, __fmul_rn(L0, fb0));
-          rl1 = fmaf(rl1, fa1, __fmul_rn(L1, fb1));
-          rm0 = mn0;
-          rm1 = mn1;
-#pragma unroll
-          for (int mt = 0; mt < KS; ++mt) {
-            racc[4 * mt + 0] = fmaf(racc[4 * mt + 0], fa0, __fmul_rn(acc[4 * mt + 0], fb0));
-            racc[4 * mt + 1] = fmaf(racc[4 * mt + 1], fa1, __fmul_rn(acc[4 * mt + 1], fb1));
-            racc[4 * mt + 2] = fmaf(racc[4 * mt + 2], fa0, __fmul_rn(acc[4 * mt + 2], fb0));
-            racc[4 * mt + 3] = fmaf(racc[4 * mt + 3], fa1, __fmul_rn(acc[4 * mt + 3], fb1));
-          }
-        };
-        // tail pool: the owner's prefix (splits 0..nse-2, in slot 0) and the pool split's
-        // partial (slot nse-1) go through L2; each side publishes, then counts itself in with a
-        // release/acquire increment, and the second one folds prefix (+) last split, which is
-        // the owned path's arithmetic in the owned path's order (bitwise the same result)
-        auto meet = [&](int slot_pub, const float* v, float m0v, float l0v, float m1v,
-                        float l1v) {
-          const int pb = (unit * p.nsplit + slot_pub) * g;
-          if (lane < 4) {
-            if (2 * qd < g) p.part_ml[pb + 2 * qd] = make_float2(m0v, l0v);
-            if (2 * qd + 1 < g) p.part_ml[pb + 2 * qd + 1] = make_float2(m1v, l1v);
-          }
-          float* q0 = p.part_acc + (size_t)(pb + 2 * qd) * D + r;
-          float* q1 = q0 + D;
-#pragma unroll
-          for (int mt = 0; mt < KS; ++mt) {
-            if (2 * qd < g) { q0[16 * mt] = v[4 * mt + 0]; q0[16 * mt + 8] = v[4 * mt + 2]; }
-            if (2 * qd + 1 < g) { q1[16 * mt] = v[4 * mt + 1]; q1[16 * mt + 8] = v[4 * mt + 3]; }
-          }
-          __syncwarp();
-          int old = 0;
-          if (lane == 0) old = atom_add_acq_rel_gpu(p.counter + unit, 1);
-          return __shfl_sync(0xffffffffu, old, 0) != 0;  // the other side is done: we fold
-        };
-        auto load_slot = [&](int slot_ld, float* v, float& m0v, float& l0v, float& m1v, float& l1v) {
-          const int pb = (unit * p.nsplit + slot_ld) * g;
-          const float2 a0 = 2 * qd < g ? __ldcg(p.part_ml + pb + 2 * qd) : make_float2(-INFINITY, 0.f);
-          const float2 a1 = 2 * qd + 1 < g ? __ldcg(p.part_ml + pb + 2 * qd + 1) : make_float2(-INFINITY, 0.f);
-          m0v = a0.x; l0v = a0.y; m1v = a1.x; l1v = a1.y;
-          const float* q0 = p.part_acc + (size_t)(pb + 2 * qd) * D + r;
-          const float* q1 = q0 + D;
-#pragma unroll
-          for (int mt = 0; mt < KS; ++mt) {
-            v[4 * mt + 0] = 2 * qd < g ? __ldcg(q0 + 16 * mt) : 0.f;
-            v[4 * mt + 2] = 2 * qd < g ? __ldcg(q0 + 16 * mt + 8) : 0.f;
-            v[4 * mt + 1] = 2 * qd + 1 < g ? __ldcg(q1 + 16 * mt) : 0.f;
-            v[4 * mt + 3] = 2 * qd + 1 < g ? __ldcg(q1 + 16 * mt + 8) : 0.f;
-          }
-        };
-        bool last = split == nse - 1;
-        if (pool) {  // the unit's last split: publish it; fold onto the prefix if that is ready
-          if (!meet(split, acc, M0, L0, M1, L1)) continue;
-          load_slot(0, racc, rm0, rl0, rm1, rl1);
-        } else if (split == 0) {
+        if (split == 0) {
           rm0 = rm1 = -INFINITY;
           rl0 = rl1 = 0.f;
 #pragma unroll
           for (int i = 0; i < KS * 4; ++i) racc[i] = 0.f;
         }
-        fold();
-        if (p.tp && !pool && split == nse - 2 && nse == p.nsplit) {  // the pool has the last split
-          if (!meet(0, racc, rm0, rl0, rm1, rl1)) continue;
-          load_slot(nse - 1, acc, M0, L0, M1, L1);
-          fold();
-          last = true;
+        float mn0, fa0, fb0, mn1, fa1, fb1;
+        merge_factors(rm0, M0, mn0, fa0, fb0);
+        merge_factors(rm1, M1, mn1, fa1, fb1);
+        rl0 = fmaf(rl0, fa0, __fmul_rn(L0, fb0));
+        rl1 = fmaf(rl1, fa1, __fmul_rn(L1, fb1));
+        rm0 = mn0;
+        rm1 = mn1;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          racc[4 * mt + 0] = fmaf(racc[4 * mt + 0], fa0, __fmul_rn(acc[4 * mt + 0], fb0));
+          racc[4 * mt + 1] = fmaf(racc[4 * mt + 1], fa1, __fmul_rn(acc[4 * mt + 1], fb1));
+          racc[4 * mt + 2] = fmaf(racc[4 * mt + 2], fa0, __fmul_rn(acc[4 * mt + 2], fb0));
+          racc[4 * mt + 3] = fmaf(racc[4 * mt + 3], fa1, __fmul_rn(acc[4 * mt + 3], fb1));
         }
-        if (last) {
+        if (split == nse - 1) {
           const float inv0 = 1.f / rl0, inv1 = 1.f / rl1;
           lse0 = rm0 + log2f(rl0);
           lse1 = rm1 + log2f(rl1);

@@ -72,9 +72,6 @@ struct DecodeParams {
   int cl;                // 1: cluster schedule -- one (unit, split) tile per CTA, the unit's nsplit
                          // CTAs form a thread-block cluster, the split partials go to the leader
                          // (cluster rank 0) through distributed shared memory, no L2 round trip
-  int tp;                // 1: tail-pool schedule (units < grid; raas_decode.cuh TileSched): CTA
-                         // b < units streams unit b's first nsplit-1 splits, the spare CTAs grab
-                         // the units' last splits, the two halves meet wait-free in L2
   int early;             // 1: the previous kernel of the stream is not this handle's decode step,
                          // so this handle's state may be read before griddepcontrol.wait
   uint32_t* req_x;       // [batch][C] table_scope 1: order-preserving max of the page scores

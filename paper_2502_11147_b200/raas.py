@@ -235,10 +235,10 @@ class RaasLayer:
         return dict(stamps=int(c[0]), decisions=int(c[1]), evictions=int(c[2]), unit_steps=int(c[3]))
 
     def raas_launch_info(self):
-        i = np.zeros(8, np.int32)
+        i = np.zeros(6, np.int32)
         _check(lib().raas_launch_info(self._h, _np_ptr(i)), "raas_launch_info")
         return dict(grid=int(i[0]), block=int(i[1]), smem=int(i[2]), split_pages=int(i[3]),
-                    nsplit=int(i[4]), cluster=int(i[5]), tail_pool=int(i[6]))
+                    nsplit=int(i[4]), cluster=int(i[5]))
 
     def close(self):
         if getattr(self, "_h", None):

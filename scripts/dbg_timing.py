@@ -75,7 +75,7 @@ print("producer end (us): min %.1f median %.1f max %.1f" % ((pe.min() - t0) / 1e
 print("combine end  (us): min %.1f median %.1f max %.1f" % ((ce.min() - t0) / 1e3, np.median(ce - t0) / 1e3, (ce.max() - t0) / 1e3))
 print("cycles/ns (SM clock GHz) ~ %.2f" % (buf[:g, 8].astype(np.float64).mean() / np.mean(pe - st)))
 
-ub2 = np.zeros((2, 4096, 4), np.uint64)
+ub2 = np.zeros((4, 4096, 4), np.uint64)
 L_.raas_debug_units.argtypes = [ctypes.c_void_p, ctypes.c_int]
 L_.raas_debug_units(ub2.ctypes.data_as(ctypes.c_void_p), ub2.size)
 ub = ub2[0, :U].astype(np.int64)
@@ -90,3 +90,9 @@ print("combine phases (us from start, median): LSE %.2f  out %.2f  stamps %.2f  
     *np.median(ph, 0), np.median(dur)))
 for u in order:
     print(f"  unit {u}: cta {ub[u,0]} pushed {push[u]:.1f} start {cs[u]:.1f} end {ce[u]:.1f}  phases {np.round(ph[u], 2)}")
+cyc = ub2[2:].reshape(4096, 8)[:U].astype(np.int64)
+print("fine marks recorded for", int((cyc[:, 6] != 0).sum()), "units")
+if cyc[:, 6].any():
+    d = np.diff(cyc[:, :7], axis=1)
+    print("combine fine marks (SM cycles, median): (none) %d, load_meta %d, load_acc %d, a5 %d, "
+          "stamp loop %d, argmin+plan %d" % tuple(np.median(d, 0)))

@@ -63,3 +63,5 @@ for k in range(8):
     print(f"{k} | {e.min():7.1f} {e.max():7.1f} | {w.min():7.1f} {w.max():7.1f} | {pe.min():7.1f} {np.median(pe):7.1f} {pe.max():7.1f}"
           f" | {ex.min():7.1f} {np.median(ex):7.1f} {ex.max():7.1f} | {busy:6.1f} | {nb/span/1e3 if prev_exit is not None else 0:6.0f}")
     prev_exit = ex.max()
+if os.environ.get("TL_DUMP"):
+    np.save(os.environ["TL_DUMP"], r)  # [launch][cta][entry, release, producer end, exit] us

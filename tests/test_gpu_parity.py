@@ -184,60 +184,6 @@ def test_cluster_schedule_bitwise_equals_default_schedule(monkeypatch, B, Hq, Hk
     assert all(np.array_equal(s0[k], s1[k]) for k in s0)
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,L,P,sp,kw", [
-    (2, 28, 4, 512, 64, 4, {}),                   # g = 7, 8 splits, from the prompt (empty pools)
-    (3, 8, 2, 256, 40, 8, {}),                    # 2 splits: the owner has only split 0
-    (2, 8, 2, 512, 40, 4, {"score_mode": 1}),     # the generic kernel (Quest scores)
-    (2, 8, 2, 512, 40, 4, {"table_scope": 1, "stamp_rule": 1, "top_r": 0.5}),
-])
-def test_tail_pool_schedule_bitwise_equals_default_schedule(monkeypatch, B, Hq, Hkv, L, P, sp, kw):
-    """The tail-pool schedule (fewer units than CTAs: CTA b streams unit b's first nsplit - 1
-    splits, spare CTAs grab the last splits, prefix and last split meet in L2) computes exactly
-    what the default schedule computes: outputs and states bitwise equal, through the fill
-    phase (last splits still empty) and the evicting phase.  RAAS_POOL=2 forces it here."""
-    st = waterfall_stream(91 + Hq + L, B, Hq, Hkv, 128, P, L // PAGE * PAGE + 3 * PAGE)
-    runs = []
-    for flag in ("0", "2"):
-        monkeypatch.setenv("RAAS_POOL", flag)
-        monkeypatch.setenv("RAAS_CLUSTER", "0")
-        layer = RaasLayer(L, 1e-4, Hq, Hkv, 128, B, split_pages=sp, **kw)
-        runs.append((layer.raas_launch_info(), *_run_gpu(st, L, Hq, Hkv, split_pages=sp, **kw)))
-    (i0, o0, s0), (i1, o1, s1) = runs
-    assert i0["tail_pool"] == 0 and i1["tail_pool"] == 1, (i0, i1)
-    assert i1["grid"] > B * Hkv
-    assert np.array_equal(o0, o1)
-    assert all(np.array_equal(s0[k], s1[k]) for k in s0)
-
-
-def test_tail_pool_schedule_at_config4_bitwise():
-    """Config 4 per GPU (32 requests x 4 kv-heads = 128 units of 8 splits): the cost model picks
-    the tail-pool schedule on all SMs; 48 steps from a full-cache waterfall state equal the
-    default schedule's (128 CTAs, one unit each) bitwise."""
-    B, Hq, Hkv, d, L, P, T = 32, 28, 4, 128, 4096, 128, 48
-    state, kst, vst, steps = waterfall_resume(404, B, Hq, Hkv, d, L, P, T, cur_count=7, lam=7.0)
-    res = []
-    for flag in ("0", "1"):
-        os.environ["RAAS_POOL"] = flag
-        try:
-            layer = RaasLayer(L, 1e-4, Hq, Hkv, d, B)
-        finally:
-            del os.environ["RAAS_POOL"]
-        layer.raas_set_state(state["t"], state["ts"], state["start"], state["count"],
-                             state["pinned"], kst, vst)
-        out = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
-        outs = []
-        for i in range(T):
-            layer.raas_decode_step(to_dev(steps.q[i]), to_dev(steps.k[i]), to_dev(steps.v[i]), out)
-            outs.append(from_dev(out))
-        res.append((layer.raas_launch_info(), np.stack(outs), layer.raas_get_state()))
-        assert layer.raas_get_status() == 0
-    (i0, o0, s0), (i1, o1, s1) = res
-    assert i0["tail_pool"] == 0 and i0["grid"] == 128, i0
-    assert i1["tail_pool"] == 1 and i1["grid"] > 128, i1
-    assert np.array_equal(o0, o1)
-    assert all(np.array_equal(s0[k], s1[k]) for k in s0)
-
-
 def test_head_sharding_bitwise():
     """Head sharding (SURVEY §8e, config 2's layout): two handles each holding half of the
     kv-heads (and their q-heads) give outputs and states bitwise equal to the unsharded handle's
