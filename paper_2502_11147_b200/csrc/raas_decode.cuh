@@ -281,6 +281,18 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   const uint32_t scr_lse = scr + MAX_SPLITS * MAX_GROUP * 8;    // float[g]
   const uint32_t scr_inv = scr_lse + MAX_GROUP * 4;             // float[g]
   const float2* ml_g = p.part_ml + (size_t)unit * p.nsplit * g;
+#ifdef RAAS_DBG_NOCOMB  // upper-bound experiment: an owned unit's combine costs ~nothing (FIFO state)
+  if (outdone) {
+    if (lane == 0) {
+      const int4 pl0 = __ldcg(p.plan + unit);
+      const int np0 = __ldg(p.npin + unit), Cc = p.C;
+      const int vic = np0 + ((pl0.x - np0 + 1) % (Cc - np0));
+      p.cnt[(size_t)unit * Cc + pl0.x] = (pl0.y & 0xffff) + 1;
+      p.plan[unit] = next_plan(pl0.x, (pl0.y & 0xffff) + 1, pl0.z, Cc, pl0.w, vic, p.status, PAGE);
+    }
+    return;
+  }
+#endif
   RAAS_CYC(0);
   RAAS_CYC(1);
   const int4 pl = __ldcg(p.plan + unit);
