@@ -57,6 +57,8 @@ template <int D, bool TOKD, bool GEN>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD, GEN>; }
 template <int D>
 constexpr auto decode_kernel_cl() { return raas::raas_decode_kernel<D, NC, S, false, false, true>; }
+template <int D>
+constexpr auto decode_kernel_q() { return raas::raas_decode_kernel<D, NC, S, false, false, false, true>; }
 // one-split units of <= 16 pages (L <= 256 at the default split size; the default method): a half-size CTA
 // (4 consumers, 8 stages, 114 KB) so that two fit on an SM and the next layer's CTA streams
 // beside the current one's tail (profiles/r02_study.md §6, §10)
@@ -76,6 +78,7 @@ struct Derived {
   int C, units, g, split_pages, nsplit;
   int Ce, ep;  // metadata entries per unit (L / page) of ep = page tokens; C = L / 16 tiles
   int tokd;    // token level with deferred stamping (page 1, threshold rule, per-head tables)
+  int qst;     // Quest scores (score_mode 1), every other option at the default: own instantiation
   int gen;     // any option beyond the default method (page 16, exact score, alpha rule,
                // per-kv-head tables, no Quest-on-prefill): the generic kernel instantiation
   int pstr;    // bf16 elements per KV page: 2 * 16 * D, + 64 (ts/start trailer) when tokd,
@@ -104,8 +107,13 @@ int derive(const raas_config* c, Derived* d) {
   d->tokd = c->page == 1 && c->stamp_rule == 0 && c->table_scope == 0 && c->score_mode == 0;
   d->qtr = c->score_mode == 1 && c->page == raas::PAGE;
   d->pstr = 2 * raas::PAGE * c->head_dim + (d->tokd ? 64 : 0) + (d->qtr ? 2 * c->head_dim : 0);
-  d->gen = !d->tokd && (c->page != raas::PAGE || c->score_mode != 0 || c->stamp_rule != 0 ||
-                        c->table_scope != 0 || c->quest_prefill_pages > 0);
+  // Quest scores with otherwise the default method: their own instantiation (the generic
+  // kernel's run-time options cost ~8 % at config 3)
+  d->qst = !d->tokd && c->score_mode == 1 && c->page == raas::PAGE && c->stamp_rule == 0 &&
+           c->table_scope == 0 && c->quest_prefill_pages == 0;
+  d->gen = !d->tokd && !d->qst &&
+           (c->page != raas::PAGE || c->score_mode != 0 || c->stamp_rule != 0 ||
+            c->table_scope != 0 || c->quest_prefill_pages > 0);
   if (c->page == 1 && c->score_mode != 0)
     return fail(RAAS_E_UNSUPPORTED, "page = 1: the representative-key bound of one key is the key itself; use score_mode 0");
   if (c->page == 1 && c->quest_prefill_pages > 0)
@@ -356,6 +364,7 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   lc.numAttrs = h->cl ? 2 : 1;
   if (h->d.tokd)     RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true, false>(), p));
   else if (h->d.gen) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, true>(), p));
+  else if (h->d.qst) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_q<D>(), p));
   else if (h->cl)    RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_cl<D>(), p));
   else if (h->half)  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_half<D>(), p));
   else               RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, false>(), p));
@@ -389,13 +398,13 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
   return best;
 }
 
-template <int D, bool TOKD, bool GEN>
+template <int D, bool TOKD, bool GEN, bool QST = false>
 int setup_kernel_t(raas_handle* h, bool want_cl) {
-  auto k = want_cl ? decode_kernel_cl<D>() : decode_kernel<D, TOKD, GEN>();
-  h->smem = Lay<D, TOKD, GEN>::SMEM;
+  auto k = want_cl ? decode_kernel_cl<D>() : QST ? decode_kernel_q<D>() : decode_kernel<D, TOKD, GEN>();
+  h->smem = Lay<D, TOKD, GEN || QST>::SMEM;  // QST: stages with room for the min / max rows
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
-  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD, GEN>::THREADS, h->smem));
+  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD, GEN || QST>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
   h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
   if (const char* e = std::getenv("RAAS_GRID")) {  // tuning experiments only (scripts/)
@@ -440,18 +449,19 @@ int setup_kernel(raas_handle* h) {
   // the leader's receive area holds nsplit partials and the unit's page maxima [C][g] fp32,
   // and its combine's preloaded metadata covers C <= 32 * CLM pages
   const long long recv_need = (long long)h->d.nsplit * Lay<D>::RECV_SLOT + 4LL * h->d.C * h->d.g;
-  bool want_cl = RAAS_CL && Lay<D>::CL_OK && !h->d.gen && h->d.nsplit >= 2 && h->d.nsplit <= 8 &&
+  bool want_cl = RAAS_CL && Lay<D>::CL_OK && !h->d.gen && !h->d.qst && h->d.nsplit >= 2 && h->d.nsplit <= 8 &&
                  tiles <= h->num_sms && recv_need <= (long long)NC * Lay<D>::DEPOSIT &&
                  h->d.C <= 32 * raas::CLM;
   if (const char* e = std::getenv("RAAS_CLUSTER")) want_cl = want_cl && std::atoi(e) != 0;
   if (h->d.gen) return setup_kernel_t<D, false, true>(h, false);
+  if (h->d.qst) return setup_kernel_t<D, false, false, true>(h, false);
   if (want_cl) {
     int rc = setup_kernel_t<D, false, false>(h, true);
     if (rc || h->cl) return rc;  // else clusters of this size do not fit: default schedule
   }
   // units of one tile of <= 16 pages: L = 256 17.8 -> 17.0 us; 32-page tiles (L = 512) lose
   // (26.4 -> 27.2 us: 8 pages per consumer on half the consumers)
-  bool want_half = h->d.nsplit == 1 && h->d.split_pages <= 16;
+  bool want_half = h->d.nsplit == 1 && h->d.split_pages <= 16 && !h->d.qst;
   if (const char* e = std::getenv("RAAS_HALF")) want_half = want_half && std::atoi(e) != 0;  // A/B, tests
   if (want_half) {
     auto k = decode_kernel_half<D>();

@@ -862,19 +862,20 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 #ifdef RAAS_DBG_TOKD_GLOBAL
 __device__ int g_tokd_dbg[16];
 #endif
-template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false>
-__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (NC <= 4 ? 2 : RAAS_MINB))
+template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false, bool QST = false>
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THREADS, (NC <= 4 ? 2 : RAAS_MINB))
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
   // CL: the cluster-schedule instantiation of the default method (small batches); the other
   // instantiations carry none of its code (registers: see DESIGN.md §6)
   // GEN = false (and !TOKD): the default method only (page = 16, exact page score, alpha rule,
   // per-kv-head tables, no Quest-on-prefill); the options' run-time branches are compiled out
   const int quest_k = GEN ? p.quest_k : 0;
-  const int score_mode = GEN ? p.score_mode : 0;
+  // QST: the Quest-score instantiation (score_mode 1 with otherwise the default method)
+  const int score_mode = GEN ? p.score_mode : (QST ? 1 : 0);
   // TOKD: the deferred token-level instantiation (p.tokd == 1); the page kernel carries none
   // of its code
   static_assert(D == 64 || D == 128, "head_dim");
-  using Lay = DecodeLayout<D, NC, S, TOKD, GEN>;
+  using Lay = DecodeLayout<D, NC, S, TOKD, GEN || QST>;
   constexpr int KS = Lay::KS, TILE = Lay::TILE, STAGE = Lay::STAGE;
   constexpr int ROW = 2 * D;  // bytes per token row
 
@@ -1504,7 +1505,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN>::THREADS, (N
                        : "memory");
           *reinterpret_cast<uint4*>(p.kvstore + (size_t)(unit * C + page) * p.pstr +
                                     ((isv ? PAGE : 0) + patch) * D + phys * 8) = val;
-          if (GEN && score_mode == 1 && !isv) {
+          if ((GEN || QST) && score_mode == 1 && !isv) {
             // the page's per-channel min / max rows (Quest representative keys, maintained on
             // write): a fresh page (row 0) restarts them from the new key
             const uint32_t ta = kb + 2 * TILE + ch * 16;
