@@ -80,6 +80,16 @@ __device__ long long g_raas_dbg_cyc[4096][8];  // combine: SM cycles at fine mar
     dbg_add(slot, t0_);                 \
   } while (0)
 
+// Checked builds (-DRAAS_CHECKED; tests/test_gpu_parity.py::test_checked_build_bounds): device
+// bounds checks on every index the step derives from its state, reported in the status word
+// (bit 8, plus bit 9 + site).  Release builds compile them out.
+#ifdef RAAS_CHECKED
+#define RAAS_CHK(cond, site) \
+  do { if (!(cond)) atomicOr(p.status, 0x100u | (1u << (9 + (site)))); } while (0)
+#else
+#define RAAS_CHK(cond, site) do {} while (0)
+#endif
+
 constexpr int PUB_ACC_OFF = MAX_GROUP * 8;  // cluster schedule: acc after the (m, l) pairs
 constexpr int FLAG_FIRST = 1;  // first page of this tile for the consuming warp
 constexpr int FLAG_LAST = 2;   // last page of this tile for the consuming warp
@@ -374,6 +384,9 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   }
   const int slot = pl.x, off = pl.y & 0xffff, evicting = pl.y >> 16;
   const int used_eff = pl.z, t = pl.w;
+  RAAS_CHK(unit >= 0 && unit < p.units && nse >= 1 && nse <= p.nsplit && slot >= 0 && slot < C &&
+               off >= 0 && off < (GEN ? p.ep : PAGE) && used_eff > slot && used_eff <= C &&
+               npin >= 0 && npin <= used_eff, 3);
   __syncwarp();
   if (!outdone && lane < g) {  // (m_s, l_s) of split s are replaced by its factors (f_a, f_b)
     float m = -INFINITY, l = 0.f;
@@ -553,6 +566,7 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   RAAS_COMB_MARK(2);
   RAAS_CYC(5);
   const int victim = warp_argmin_page(best);
+  RAAS_CHK(victim >= -1 && victim < C && (victim < 0 || victim >= npin), 4);
   n_stamp = warp_sum_i(n_stamp);
   n_dec = warp_sum_i(n_dec);
   RAAS_COMB_MARK(3);
@@ -1061,6 +1075,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THRE
         const int s = (int)(jj % S);
         RAAS_TIMED(1, mbar_wait(empty(s), ((jj / S) & 1) ^ 1));
         // the tile the new token goes to, its row count and the row it is written to
+        RAAS_CHK(unit >= 0 && unit < p.units && page >= 0 && page < C && c >= 0 && c <= PAGE, 0);
         const bool is_slot = TOKD ? false : tok ? page == (slot >> 4) : page == slot;
         const int patch = !is_slot ? -1 : (tok ? (slot & (PAGE - 1)) : off);
         sinfo[2 * s] = make_int4(unit, page, (is_slot && !tok) ? off + 1 : c, patch);
@@ -1213,6 +1228,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THRE
         break;
       }
       const int unit = t0.x, split = t0.y, nse = t0.z, n = t0.w, J = t1.x, owned = t1.z;
+      RAAS_CHK(unit >= 0 && unit < p.units && split >= 0 && split < nse && nse <= p.nsplit &&
+                   n > 0 && n <= p.split_pages, 2);
       const int nw = min(n, NC);
       float acc[KS * 4];
 #pragma unroll
@@ -1438,6 +1455,8 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THRE
         continue;
       }
       const int unit = i0.x, page = i0.y, cnt = i0.z, patch = i0.w, k = i1.x, par = k & 1;
+      RAAS_CHK(unit >= 0 && unit < p.units && page >= 0 && page < C && cnt >= 0 && cnt <= PAGE &&
+                   patch >= -1 && patch < PAGE, 1);
       const uint32_t kb = ring + s * STAGE, vb = kb + TILE;
 
       if (flags & FLAG_FIRST) {  // fresh softmax state; this unit's q fragments from smem

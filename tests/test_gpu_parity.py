@@ -571,6 +571,28 @@ def test_compute_sanitizer(tool):
     assert "ERROR SUMMARY: 0 errors" in r.stdout or "(0 errors, 0 warnings)" in r.stdout
 
 
+@pytest.mark.slow
+def test_checked_build_bounds():
+    """Device bounds checks instead of compute-sanitizer (refused by the GPU pool): a build with
+    -DRAAS_CHECKED checks every page / unit / slot / split index the step derives from its state
+    (status word bit 8 + site) and runs the sanitizer cases (toy, multi-tile, per-request tables,
+    token level, cluster schedule, early start, host path) plus full-size steps of configs 2-5
+    and the method variants: every status must stay 0."""
+    import subprocess
+    import sys
+
+    from paper_2502_11147_b200 import build
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "build"), exist_ok=True)
+    lib = build.build(out=os.path.join(root, "build", "libraas_checked.so"), defines=["RAAS_CHECKED"])
+    env = dict(os.environ, RAAS_LIB=lib)
+    for script, ok in (("sanitize_case.py", "sanitize early/host ok"), ("checked_case.py", "checked cases ok")):
+        r = subprocess.run([sys.executable, os.path.join(root, "scripts", script)], env=env,
+                           capture_output=True, text=True, timeout=1200)
+        assert r.returncode == 0 and ok in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 # ------------------------------------------------------------------ NEXT-1: Quest bound mode
 
 
