@@ -57,8 +57,9 @@ template <int D, bool TOKD, bool GEN>
 constexpr auto decode_kernel() { return raas::raas_decode_kernel<D, NC, S, TOKD, GEN>; }
 template <int D>
 constexpr auto decode_kernel_cl() { return raas::raas_decode_kernel<D, NC, S, false, false, true>; }
-template <int D>
-constexpr auto decode_kernel_q() { return raas::raas_decode_kernel<D, NC, S, false, false, false, true>; }
+// one option beside the default method compiled in (raas::F_QUEST / F_TOPR / F_TSC / F_HYB)
+template <int D, int FM>
+constexpr auto decode_kernel_f() { return raas::raas_decode_kernel<D, NC, S, false, false, false, FM>; }
 // one-split units of <= 16 pages (L <= 256 at the default split size; the default method): a half-size CTA
 // (4 consumers, 8 stages, 114 KB) so that two fit on an SM and the next layer's CTA streams
 // beside the current one's tail (profiles/r02_study.md §6, §10)
@@ -78,7 +79,7 @@ struct Derived {
   int C, units, g, split_pages, nsplit;
   int Ce, ep;  // metadata entries per unit (L / page) of ep = page tokens; C = L / 16 tiles
   int tokd;    // token level with deferred stamping (page 1, threshold rule, per-head tables)
-  int qst;     // Quest scores (score_mode 1), every other option at the default: own instantiation
+  int fm;      // exactly one option beside the default method (raas::F_*): its own instantiation
   int gen;     // any option beyond the default method (page 16, exact score, alpha rule,
                // per-kv-head tables, no Quest-on-prefill): the generic kernel instantiation
   int pstr;    // bf16 elements per KV page: 2 * 16 * D, + 64 (ts/start trailer) when tokd,
@@ -107,11 +108,12 @@ int derive(const raas_config* c, Derived* d) {
   d->tokd = c->page == 1 && c->stamp_rule == 0 && c->table_scope == 0 && c->score_mode == 0;
   d->qtr = c->score_mode == 1 && c->page == raas::PAGE;
   d->pstr = 2 * raas::PAGE * c->head_dim + (d->tokd ? 64 : 0) + (d->qtr ? 2 * c->head_dim : 0);
-  // Quest scores with otherwise the default method: their own instantiation (the generic
-  // kernel's run-time options cost ~8 % at config 3)
-  d->qst = !d->tokd && c->score_mode == 1 && c->page == raas::PAGE && c->stamp_rule == 0 &&
-           c->table_scope == 0 && c->quest_prefill_pages == 0;
-  d->gen = !d->tokd && !d->qst &&
+  // exactly one option beside the default method (page 16): its own instantiation with the
+  // option compiled in (the generic kernel's run-time options cost 5-8 % at config 3)
+  const int fm = (c->score_mode == 1 ? raas::F_QUEST : 0) | (c->stamp_rule == 1 ? raas::F_TOPR : 0) |
+                 (c->table_scope != 0 ? raas::F_TSC : 0) | (c->quest_prefill_pages > 0 ? raas::F_HYB : 0);
+  d->fm = (!d->tokd && c->page == raas::PAGE && (fm & (fm - 1)) == 0) ? fm : 0;
+  d->gen = !d->tokd && d->fm == 0 &&
            (c->page != raas::PAGE || c->score_mode != 0 || c->stamp_rule != 0 ||
             c->table_scope != 0 || c->quest_prefill_pages > 0);
   if (c->page == 1 && c->score_mode != 0)
@@ -364,7 +366,10 @@ int launch_decode(raas_handle* h, const void* q, const void* k_new, const void* 
   lc.numAttrs = h->cl ? 2 : 1;
   if (h->d.tokd)     RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, true, false>(), p));
   else if (h->d.gen) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, true>(), p));
-  else if (h->d.qst) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_q<D>(), p));
+  else if (h->d.fm == raas::F_QUEST) RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_f<D, raas::F_QUEST>(), p));
+  else if (h->d.fm == raas::F_TOPR)  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_f<D, raas::F_TOPR>(), p));
+  else if (h->d.fm == raas::F_TSC)   RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_f<D, raas::F_TSC>(), p));
+  else if (h->d.fm == raas::F_HYB)   RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_f<D, raas::F_HYB>(), p));
   else if (h->cl)    RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_cl<D>(), p));
   else if (h->half)  RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel_half<D>(), p));
   else               RAAS_CUDA(cudaLaunchKernelEx(&lc, decode_kernel<D, false, false>(), p));
@@ -398,13 +403,14 @@ int choose_grid(int units, int nsplit, int sp, int cap) {
   return best;
 }
 
-template <int D, bool TOKD, bool GEN, bool QST = false>
+template <int D, bool TOKD, bool GEN, int FM = 0>
 int setup_kernel_t(raas_handle* h, bool want_cl) {
-  auto k = want_cl ? decode_kernel_cl<D>() : QST ? decode_kernel_q<D>() : decode_kernel<D, TOKD, GEN>();
-  h->smem = Lay<D, TOKD, GEN || QST>::SMEM;  // QST: stages with room for the min / max rows
+  auto k = want_cl ? decode_kernel_cl<D>() : FM ? decode_kernel_f<D, FM>() : decode_kernel<D, TOKD, GEN>();
+  constexpr bool QTR = GEN || (FM & raas::F_QUEST);  // stages with room for the min / max rows
+  h->smem = Lay<D, TOKD, QTR>::SMEM;
   RAAS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
   int per_sm = 0;
-  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD, GEN || QST>::THREADS, h->smem));
+  RAAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Lay<D, TOKD, QTR>::THREADS, h->smem));
   if (per_sm < 1) return fail(RAAS_E_CUDA, "decode kernel does not fit on an SM");
   h->grid = choose_grid(h->d.units, h->d.nsplit, h->d.split_pages, h->num_sms * per_sm);
   if (const char* e = std::getenv("RAAS_GRID")) {  // tuning experiments only (scripts/)
@@ -449,19 +455,22 @@ int setup_kernel(raas_handle* h) {
   // the leader's receive area holds nsplit partials and the unit's page maxima [C][g] fp32,
   // and its combine's preloaded metadata covers C <= 32 * CLM pages
   const long long recv_need = (long long)h->d.nsplit * Lay<D>::RECV_SLOT + 4LL * h->d.C * h->d.g;
-  bool want_cl = RAAS_CL && Lay<D>::CL_OK && !h->d.gen && !h->d.qst && h->d.nsplit >= 2 && h->d.nsplit <= 8 &&
+  bool want_cl = RAAS_CL && Lay<D>::CL_OK && !h->d.gen && !h->d.fm && h->d.nsplit >= 2 && h->d.nsplit <= 8 &&
                  tiles <= h->num_sms && recv_need <= (long long)NC * Lay<D>::DEPOSIT &&
                  h->d.C <= 32 * raas::CLM;
   if (const char* e = std::getenv("RAAS_CLUSTER")) want_cl = want_cl && std::atoi(e) != 0;
   if (h->d.gen) return setup_kernel_t<D, false, true>(h, false);
-  if (h->d.qst) return setup_kernel_t<D, false, false, true>(h, false);
+  if (h->d.fm == raas::F_QUEST) return setup_kernel_t<D, false, false, raas::F_QUEST>(h, false);
+  if (h->d.fm == raas::F_TOPR) return setup_kernel_t<D, false, false, raas::F_TOPR>(h, false);
+  if (h->d.fm == raas::F_TSC) return setup_kernel_t<D, false, false, raas::F_TSC>(h, false);
+  if (h->d.fm == raas::F_HYB) return setup_kernel_t<D, false, false, raas::F_HYB>(h, false);
   if (want_cl) {
     int rc = setup_kernel_t<D, false, false>(h, true);
     if (rc || h->cl) return rc;  // else clusters of this size do not fit: default schedule
   }
   // units of one tile of <= 16 pages: L = 256 17.8 -> 17.0 us; 32-page tiles (L = 512) lose
   // (26.4 -> 27.2 us: 8 pages per consumer on half the consumers)
-  bool want_half = h->d.nsplit == 1 && h->d.split_pages <= 16 && !h->d.qst;
+  bool want_half = h->d.nsplit == 1 && h->d.split_pages <= 16 && !h->d.fm;
   if (const char* e = std::getenv("RAAS_HALF")) want_half = want_half && std::atoi(e) != 0;  // A/B, tests
   if (want_half) {
     auto k = decode_kernel_half<D>();

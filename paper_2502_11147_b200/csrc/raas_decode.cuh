@@ -267,7 +267,11 @@ struct DecodeLayout {
 // ---------------------------------------------------------------------------------------------
 // a5-a7 for one unit, by one warp, after all its splits have published their partials.
 // ---------------------------------------------------------------------------------------------
-template <int D, bool GEN>
+// Feature masks of the specialised instantiations (one option beside the default method each;
+// GEN decides every option at run time): Quest scores, top-r rule, per-request tables, hybrid
+constexpr int F_QUEST = 1, F_TOPR = 2, F_TSC = 4, F_HYB = 8;
+
+template <int D, bool GEN, int FM = 0>
 __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, int nse, uint32_t scr,
                                              int lane, bool outdone, bool CL = false, uint32_t pub = 0,
                                              uint32_t clbar = 0) {
@@ -280,8 +284,8 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
   // outdone: the merge warp already folded the splits and wrote out; the LSE is in scr_lse
   // GEN = false: the default method (page = 16, alpha rule, one table per kv-head) with the
   // optional rules compiled out; GEN = true: every option decided at run time
-  const bool tscope = GEN && p.table_scope != 0;
-  const bool topr = GEN && p.stamp_rule == 1;
+  const bool tscope = (GEN || (FM & F_TSC)) && p.table_scope != 0;
+  const bool topr = (GEN || (FM & F_TOPR)) && p.stamp_rule == 1;
   // Latency-oriented: the plan, the split statistics, the first block of split partials and
   // the first 128 pages' metadata are all requested before any of them is used (nse comes with
   // the queue entry), so a unit costs ~one dependent L2 round trip before its stores.
@@ -876,20 +880,22 @@ __device__ __forceinline__ void combine_unit_tok(const DecodeParams& p, int unit
 #ifdef RAAS_DBG_TOKD_GLOBAL
 __device__ int g_tokd_dbg[16];
 #endif
-template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false, bool QST = false>
-__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THREADS, (NC <= 4 ? 2 : RAAS_MINB))
+template <int D, int NC, int S, bool TOKD, bool GEN, bool CL = false, int FM = 0>
+__global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || (FM & F_QUEST)>::THREADS,
+                                  (NC <= 4 ? 2 : RAAS_MINB))
     raas_decode_kernel(const __grid_constant__ DecodeParams p) {
   // CL: the cluster-schedule instantiation of the default method (small batches); the other
   // instantiations carry none of its code (registers: see DESIGN.md §6)
   // GEN = false (and !TOKD): the default method only (page = 16, exact page score, alpha rule,
   // per-kv-head tables, no Quest-on-prefill); the options' run-time branches are compiled out
-  const int quest_k = GEN ? p.quest_k : 0;
-  // QST: the Quest-score instantiation (score_mode 1 with otherwise the default method)
-  const int score_mode = GEN ? p.score_mode : (QST ? 1 : 0);
+  // FM: a specialised instantiation with one option compiled in (F_QUEST: Quest scores, F_TOPR:
+  // top-r rule, F_TSC: per-request tables, F_HYB: Quest-on-prefill hybrid), the rest default
+  const int quest_k = (GEN || (FM & F_HYB)) ? p.quest_k : 0;
+  const int score_mode = GEN ? p.score_mode : ((FM & F_QUEST) ? 1 : 0);
   // TOKD: the deferred token-level instantiation (p.tokd == 1); the page kernel carries none
   // of its code
   static_assert(D == 64 || D == 128, "head_dim");
-  using Lay = DecodeLayout<D, NC, S, TOKD, GEN || QST>;
+  using Lay = DecodeLayout<D, NC, S, TOKD, GEN || (FM & F_QUEST)>;
   constexpr int KS = Lay::KS, TILE = Lay::TILE, STAGE = Lay::STAGE;
   constexpr int ROW = 2 * D;  // bytes per token row
 
@@ -1010,7 +1016,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THRE
       if (lane == 0 && unit < 4096) { g_raas_dbg_unit[unit][0] = blockIdx.x; g_raas_dbg_unit[unit][2] = dbg_gtimer(); }
 #endif
       if constexpr (TOKD) combine_unit_tok<D>(p, unit, nse_u, scratch, lane);
-      else        combine_unit<D, GEN>(p, unit, nse_u, scratch, lane, outdone, cl, recv, clfull);
+      else        combine_unit<D, GEN, FM>(p, unit, nse_u, scratch, lane, outdone, cl, recv, clfull);
 #ifdef RAAS_DBG_TIMING
       if (lane == 0 && unit < 4096) g_raas_dbg_unit[unit][3] = dbg_gtimer();
 #endif
@@ -1524,7 +1530,7 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || QST>::THRE
                        : "memory");
           *reinterpret_cast<uint4*>(p.kvstore + (size_t)(unit * C + page) * p.pstr +
                                     ((isv ? PAGE : 0) + patch) * D + phys * 8) = val;
-          if ((GEN || QST) && score_mode == 1 && !isv) {
+          if ((GEN || (FM & F_QUEST)) && score_mode == 1 && !isv) {
             // the page's per-channel min / max rows (Quest representative keys, maintained on
             // write): a fresh page (row 0) restarts them from the new key
             const uint32_t ta = kb + 2 * TILE + ch * 16;

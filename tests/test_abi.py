@@ -63,8 +63,8 @@ def test_sass_cluster_instantiation_uses_cluster_barriers(L):
     def sass(fn):
         return subprocess.run([cuobjdump, "-sass", "-fun", fn, raas.LIB_PATH], capture_output=True,
                               text=True).stdout
-    cl = sass("_ZN4raas18raas_decode_kernelILi128ELi8ELi16ELb0ELb0ELb1ELb0EEEvNS_12DecodeParamsE")
-    lean = sass("_ZN4raas18raas_decode_kernelILi128ELi8ELi16ELb0ELb0ELb0ELb0EEEvNS_12DecodeParamsE")
+    cl = sass("_ZN4raas18raas_decode_kernelILi128ELi8ELi16ELb0ELb0ELb1ELi0EEEvNS_12DecodeParamsE")
+    lean = sass("_ZN4raas18raas_decode_kernelILi128ELi8ELi16ELb0ELb0ELb0ELi0EEEvNS_12DecodeParamsE")
     assert "UCGABAR_ARV" in cl and "UCGABAR_WAIT" in cl and "SYNCS.ARRIVE.TRANS64.RED" in cl
     assert "HMMA.16816.F32.BF16" in cl and "UBLKCP" in cl
     assert lean and "UCGABAR" not in lean
