@@ -113,6 +113,8 @@ int derive(const raas_config* c, Derived* d) {
   const int fm = (c->score_mode == 1 ? raas::F_QUEST : 0) | (c->stamp_rule == 1 ? raas::F_TOPR : 0) |
                  (c->table_scope != 0 ? raas::F_TSC : 0) | (c->quest_prefill_pages > 0 ? raas::F_HYB : 0);
   d->fm = (!d->tokd && c->page == raas::PAGE && (fm & (fm - 1)) == 0) ? fm : 0;
+  if (const char* e = std::getenv("RAAS_GENERIC"))  // tests: the generic kernel for every option
+    if (std::atoi(e) != 0) d->fm = 0;
   d->gen = !d->tokd && d->fm == 0 &&
            (c->page != raas::PAGE || c->score_mode != 0 || c->stamp_rule != 0 ||
             c->table_scope != 0 || c->quest_prefill_pages > 0);

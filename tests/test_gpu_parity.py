@@ -184,6 +184,27 @@ def test_cluster_schedule_bitwise_equals_default_schedule(monkeypatch, B, Hq, Hk
     assert all(np.array_equal(s0[k], s1[k]) for k in s0)
 
 
+@pytest.mark.parametrize("kw,P", [
+    ({"score_mode": 1}, 40),
+    ({"stamp_rule": 1, "top_r": 0.5}, 40),
+    ({"table_scope": 1}, 40),
+    ({"quest_prefill_pages": 2}, 100),
+])
+def test_specialised_kernel_bitwise_equals_generic_kernel(monkeypatch, kw, P):
+    """A handle with exactly one option beside the default method runs its own instantiation
+    (the option compiled in); RAAS_GENERIC=1 forces the generic kernel that decides every option
+    at run time.  Outputs and states are bitwise equal through the fill and evicting phases."""
+    B, Hq, Hkv, L = 2, 8, 2, 256
+    st = waterfall_stream(131 + P, B, Hq, Hkv, 128, P, L + 3 * PAGE)
+    runs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("RAAS_GENERIC", flag)
+        runs.append(_run_gpu(st, L, Hq, Hkv, split_pages=4, **kw))
+    (o0, s0), (o1, s1) = runs
+    assert np.array_equal(o0, o1)
+    assert all(np.array_equal(s0[k], s1[k]) for k in s0)
+
+
 def test_head_sharding_bitwise():
     """Head sharding (SURVEY §8e, config 2's layout): two handles each holding half of the
     kv-heads (and their q-heads) give outputs and states bitwise equal to the unsharded handle's
