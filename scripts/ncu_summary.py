@@ -74,11 +74,23 @@ def stall_by_line(rep, lib, kernel_regex):
     return agg
 
 
+def mangled_from_report(rep):
+    """Mangled name of the profiled raas_decode_kernel instantiation, from the report's demangled
+    'raas_decode_kernel<128, 8, 16, 0, 0, 0, 0>' (D, NC, S, TOKD, GEN, CL[, FM])."""
+    rows = list(csv.reader(io.StringIO(ncu(["-i", rep, "--page", "raw", "--csv"]))))
+    name = rows[2][rows[0].index("Kernel Name")]
+    args = [int(x) for x in re.search(r"<([^>]*)>", name).group(1).split(",")]
+    kinds = ["i", "i", "i", "b", "b", "b", "i"][:len(args)]
+    body = "".join(f"L{k}{v}E" for k, v in zip(kinds, args))
+    return f"_ZN4raas18raas_decode_kernelI{body}EEvNS_12DecodeParamsE"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--lib", default="paper_2502_11147_b200/libraas.so")
-    ap.add_argument("--kernel", default="_ZN4raas18raas_decode_kernelILi128")
+    ap.add_argument("--kernel", default="",
+                    help="mangled-name regex of the profiled instantiation (default: from the report)")
     ap.add_argument("--top", type=int, default=25)
     a = ap.parse_args()
     m = raw_metrics(a.rep)
@@ -92,8 +104,10 @@ def main():
     print("\n## stall reasons (pc samples)")
     for k, v in sorted(st.items(), key=lambda x: -x[1])[:12]:
         print(f"- {k}: {v} ({100 * v / tot:.1f}%)")
+    kern = a.kernel or mangled_from_report(a.rep)
+    print(f"\n(source lines mapped through {kern} in {a.lib})")
     try:
-        agg = stall_by_line(a.rep, a.lib, a.kernel)
+        agg = stall_by_line(a.rep, a.lib, re.escape(kern) if not a.kernel else kern)
     except Exception as e:  # pragma: no cover
         print("(no line mapping:", e, ")")
         return
