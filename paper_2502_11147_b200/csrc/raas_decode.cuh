@@ -1658,17 +1658,11 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || (FM & F_QU
           const unsigned long long key = valid ? cand_key(tsv, stv) : ~0ull;
           if (key < kmin) { kmin = key; rmin = row; }
         }
-        // page minimum over the 8 row lanes (keys are unique: start positions differ)
-        unsigned long long pk = kmin;
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-          const unsigned long long w2 = __shfl_xor_sync(0xffffffffu, pk, o);
-          pk = w2 < pk ? w2 : pk;
-        }
-        if (pk < ckey) {  // warp-uniform; the lane (and row) holding the page minimum
-          const unsigned hit = __ballot_sync(0xffffffffu, kmin == pk);
-          ckey = pk;
-          cslot = page * PAGE + __shfl_sync(0xffffffffu, rmin, __ffs(hit) - 1);
+        // this lane's running minimum over its rows of the tile (reduced over the warp once,
+        // at the tile's last page; keys are unique: start positions differ)
+        if (kmin < ckey) {
+          ckey = kmin;
+          cslot = page * PAGE + rmin;
         }
       }
       float s0 = (c0[0] + c1[0]) * p.scale_log2, s1 = (c0[1] + c1[1]) * p.scale_log2;
@@ -1826,6 +1820,18 @@ __global__ void __launch_bounds__(DecodeLayout<D, NC, S, TOKD, GEN || (FM & F_QU
         sts_f32(dep + 128 * (KS * 4 + 1), m1);
         sts_f32(dep + 128 * (KS * 4 + 2), l0);
         sts_f32(dep + 128 * (KS * 4 + 3), l1);
+        if constexpr (TOKD) {  // the warp's minimum over its lanes' running minima
+          unsigned long long wk = ckey;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long w2 = __shfl_xor_sync(0xffffffffu, wk, o);
+            wk = w2 < wk ? w2 : wk;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, ckey == wk);
+          const int ws = __shfl_sync(0xffffffffu, cslot, __ffs(hit) - 1);
+          ckey = wk;
+          cslot = wk == ~0ull ? -1 : ws;
+        }
         if (TOKD && lane == 0) {  // the tile's victim candidate of this warp
           asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(cand + (par * NC + w) * 16),
                        "r"(static_cast<uint32_t>(ckey)), "r"(static_cast<uint32_t>(ckey >> 32)),
