@@ -391,6 +391,7 @@ def test_full_size_sampled_units_lockstep(oracle_mod, cfg, B, Hq, Hkv, L, P, sp,
     ({"stamp_rule": 1, "top_r": 0.5}, 7.0),                  # NEXT-3 top-r (r = 0.5, :135)
     ({"table_scope": 1}, 11.0),                              # NEXT-2 one table per request (38 %)
     ({"table_scope": 1, "stamp_rule": 1, "top_r": 0.5}, 7.0),
+    ({"quest_prefill_pages": 16}, 7.0),                      # NEXT-4 hybrid, P = 1024 (as benched)
 ])
 def test_full_size_variants_sampled_lockstep(oracle_mod, kw, lam):
     """The method variants in bench.py's launch configuration at config 3 (B = 64, L = 2048,
@@ -398,6 +399,8 @@ def test_full_size_variants_sampled_lockstep(oracle_mod, kw, lam):
     on the oracle in lockstep for 40 steps (per-request tables: every kv-head of a request starts
     from the same replica)."""
     B, Hq, Hkv, d, L, P, T = 64, 32, 8, 128, 2048, 256, 40
+    if kw.get("quest_prefill_pages"):
+        P = 1024  # 64 full prompt pages, K = 16 of them attended per step (bench.py --P 1024)
     state, kst, vst, steps = waterfall_resume(500 + int(lam), B, Hq, Hkv, d, L, P, T, cur_count=9, lam=lam)
     if kw.get("table_scope"):
         for k in ("t", "ts", "start", "count", "pinned"):
