@@ -735,6 +735,11 @@ int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_
   const void* km = mapped_alias(k_new_host, 16);
   const void* vm = mapped_alias(v_new_host, 16);
   void* om = mapped_alias(out_host, 8);
+#ifdef RAAS_DBG_E2E  // e2e breakdown experiment: 1 = out to device (no host write), 2 = no ingest
+  static const int dbg_e2e = std::getenv("RAAS_DBG_E2E") ? std::atoi(std::getenv("RAAS_DBG_E2E")) : 0;
+  if (dbg_e2e == 1) om = a + h->lay.so;
+  if (dbg_e2e == 2) qm = km = vm = nullptr;
+#endif
   if (qm && km && vm) {
     // pinned inputs: one zero-copy ingest kernel (PCIe reads overlap the previous kernel)
     const int nq = (int)(U * g * D * 2 / 16), nkv = (int)(U * D * 2 / 16);
@@ -753,7 +758,11 @@ int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_
                                  static_cast<const uint4*>(km), static_cast<const uint4*>(vm),
                                  reinterpret_cast<uint4*>(a + h->lay.sq), reinterpret_cast<uint4*>(a + h->lay.sk),
                                  reinterpret_cast<uint4*>(a + h->lay.sv), nq, nkv));
-  } else {  // pageable inputs: staged copies
+  } else
+#ifdef RAAS_DBG_E2E
+  if (dbg_e2e != 2)
+#endif
+  {  // pageable inputs: staged copies
     RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sq, q_host, U * g * D * 2, cudaMemcpyHostToDevice, st));
     RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sk, k_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
     RAAS_CUDA(cudaMemcpyAsync(a + h->lay.sv, v_new_host, U * D * 2, cudaMemcpyHostToDevice, st));
