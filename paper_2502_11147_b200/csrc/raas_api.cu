@@ -265,6 +265,13 @@ namespace {
 std::mutex g_last_mu;
 std::unordered_map<cudaStream_t, const raas_handle*> g_last_decode;
 
+// true when the last decode launched on `st` is not h's (or there is none); no update
+bool other_last(const raas_handle* h, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_last_mu);
+  auto it = g_last_decode.find(st);
+  return !(it != g_last_decode.end() && it->second == h);
+}
+
 bool note_launch(const raas_handle* h, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_last_mu);
   auto it = g_last_decode.find(st);
@@ -757,7 +764,8 @@ int raas_decode_step_host(raas_handle* h, const void* q_host, const void* k_new_
     RAAS_CUDA(cudaLaunchKernelEx(&lc, raas::raas_ingest_kernel, static_cast<const uint4*>(qm),
                                  static_cast<const uint4*>(km), static_cast<const uint4*>(vm),
                                  reinterpret_cast<uint4*>(a + h->lay.sq), reinterpret_cast<uint4*>(a + h->lay.sk),
-                                 reinterpret_cast<uint4*>(a + h->lay.sv), nq, nkv));
+                                 reinterpret_cast<uint4*>(a + h->lay.sv), nq, nkv,
+                                 other_last(h, st) ? 1 : 0));
   } else
 #ifdef RAAS_DBG_E2E
   if (dbg_e2e != 2)

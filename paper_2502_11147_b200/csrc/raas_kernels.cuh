@@ -542,7 +542,8 @@ __global__ void __launch_bounds__(QSEL_THREADS) raas_qselect_kernel(const __nv_b
 constexpr int INGEST_THREADS = 128, INGEST_PER = 4;
 __global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
     const uint4* __restrict__ q_h, const uint4* __restrict__ k_h, const uint4* __restrict__ v_h,
-    uint4* __restrict__ q_d, uint4* __restrict__ k_d, uint4* __restrict__ v_d, int nq, int nkv) {
+    uint4* __restrict__ q_d, uint4* __restrict__ k_d, uint4* __restrict__ v_d, int nq, int nkv,
+    int store_early) {
   const int total = nq + 2 * nkv;
   const int nth = gridDim.x * INGEST_THREADS;
   const int tid = blockIdx.x * INGEST_THREADS + threadIdx.x;
@@ -556,7 +557,11 @@ __global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
   };
   // the decode step may start (its state reads and first page copies) at once: it reads q /
   // k_new / v_new only after its own griddepcontrol.wait, i.e. after this grid has completed,
-  // and this grid completes only after the previous kernel of the stream (our wait below)
+  // and this grid completes only after the previous kernel of the stream (our wait below).
+  // store_early (the previous decode launch on the stream is another handle's, so nothing still
+  // running reads this handle's staging buffers): the whole copy runs before the wait, which
+  // then only keeps the chain ordered; otherwise the stores wait (a handle stepped twice in a
+  // row: its previous decode may still read q from the staging buffer)
   pdl_launch_dependents();
   uint4 r[INGEST_PER];
 #pragma unroll
@@ -564,7 +569,7 @@ __global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
     const int i = tid + j * nth;
     if (i < total) r[j] = ld(i);
   }
-  pdl_wait();
+  if (!store_early) pdl_wait();
 #pragma unroll
   for (int j = 0; j < INGEST_PER; ++j) {
     const int i = tid + j * nth;
@@ -582,6 +587,7 @@ __global__ void __launch_bounds__(INGEST_THREADS) raas_ingest_kernel(
       if (i < total) st(i, r[j]);
     }
   }
+  if (store_early) pdl_wait();  // completes only after the previous kernel: the chain holds
 }
 
 }  // namespace raas
