@@ -307,6 +307,13 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     return;
   }
 #endif
+#ifdef RAAS_DBG_COMBDELAY  // sensitivity probe: a longer owned-unit combine
+  if (outdone) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < RAAS_DBG_COMBDELAY) {
+    }
+  }
+#endif
   RAAS_CYC(0);
   RAAS_CYC(1);
   const int4 pl = __ldcg(p.plan + unit);
