@@ -23,6 +23,11 @@
 //   warps 3..NC+2  consumers: ring position j goes to consumer j % NC; per page
 //                  S^T = K_page Q^T and O^T += V_page^T P^T on mma.sync m16n8k16 (16 tokens = M,
 //                  the <= 8 q-heads of the GQA group = N), online softmax in fp32 registers.
+//
+// Instantiations (template <D, NC, S, TOKD, GEN, CL, FM>, chosen per handle in raas_api.cu):
+// lean (the default method, options compiled out); FM = F_QUEST / F_TOPR / F_TSC / F_HYB (one
+// option compiled in); GEN (every option decided at run time); TOKD (deferred token level);
+// CL (cluster schedule of lean for small batches); NC = 4, S = 8 (half-size CTAs, L <= 256).
 #pragma once
 
 #ifndef RAAS_MINB
