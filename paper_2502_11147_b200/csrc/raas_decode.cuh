@@ -312,8 +312,12 @@ __device__ __forceinline__ void combine_unit(const DecodeParams& p, int unit, in
     return;
   }
 #endif
-#ifdef RAAS_DBG_COMBDELAY  // sensitivity probe: a longer owned-unit combine
+#ifdef RAAS_DBG_COMBDELAY  // sensitivity probe: a longer owned-unit (or, _SH, shared-unit) combine
+#ifdef RAAS_DBG_COMBDELAY_SH
+  if (!outdone) {
+#else
   if (outdone) {
+#endif
     const long long t0 = clock64();
     while (clock64() - t0 < RAAS_DBG_COMBDELAY) {
     }
